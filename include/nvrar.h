@@ -1,0 +1,177 @@
+/*
+ * nvrar.h — C ABI of the B200-native NVRAR all-reduce (libnvrar_b200.so).
+ *
+ * This is the drop-in boundary for the reference's all-reduce path. The
+ * reference (/root/reference/proj, a header-only C++20 library) exposes the
+ * path as a per-rank C++ object; each entry point below replaces one piece of
+ * it:
+ *
+ *   reference                                            | this ABI
+ *   -----------------------------------------------------+-----------------------------
+ *   NvrarAllreduce<T>(Ctx&, max_elems)  nvrar.hpp:44-78  | nvrar_init / nvrar_comm_create
+ *     + ClusterTopology{nodes,gpus}     topology.hpp:24-48 |   + nvrar_comm_export
+ *     + Ctx::alloc_region (symmetric)   transport.hpp:146-148 |   + nvrar_comm_connect
+ *   Ctx::alloc_region for caller data   transport.hpp:146-148 | nvrar_alloc_symmetric
+ *   NvrarAllreduce<T>::run(in,out,cfg)  nvrar.hpp:84-129 | nvrar_allreduce
+ *   NvrarConfig{blocks,chunk_bytes}     fused.hpp:106-116 | nvrar_set_config
+ *   NvrarAllreduce<T>::sequence()       nvrar.hpp:80     | nvrar_get_sequence
+ *   NvrarAllreduce<T>::peers()          nvrar.hpp:158    | nvrar_get_peers
+ *   run_ranks(...) all ranks in 1 process run.hpp:15-24  | nvrar_allreduce_local (all
+ *                                                        |   comms of one device, one launch)
+ *   ~NvrarAllreduce / engine teardown                    | nvrar_finalize
+ *   exceptions (errors.hpp:15-85), DeadlockError blocked | nvrar_status_t, nvrar_last_error,
+ *     set (errors.hpp:46-85)                             |   nvrar_get_blocked
+ *
+ * Status codes map the reference's exception classes one to one:
+ *   InvalidArgumentError  -> NVRAR_ERR_INVALID_ARGUMENT
+ *   InvalidTopologyError  -> NVRAR_ERR_INVALID_TOPOLOGY
+ *   ProtocolFaultError    -> NVRAR_ERR_PROTOCOL_FAULT  (length mismatch, stale/future flag)
+ *   DeadlockError         -> NVRAR_ERR_DEADLOCK        (device watchdog; see nvrar_get_blocked)
+ *
+ * Semantics kept from the reference: global rank =
+ * node*gpus_per_node + local; nodes must be a power of two; sum only; int32
+ * adds wrap; fp32 results are bit-identical to NvrarAllreduce<float> for the
+ * same (nodes, gpus_per_node); bf16 results equal the fp32 reference on the
+ * up-cast inputs rounded once to bf16; every call (count == 0 included) bumps
+ * the sequence number by one; all ranks must issue the same calls with equal
+ * counts (a mismatch across an XOR-peer or flat-schedule pair is a protocol
+ * fault). Calls are asynchronous and ordered on `stream`; device-side faults
+ * are sticky and surface through nvrar_check().
+ *
+ * No torch or CUDA types appear here: streams and device pointers are plain
+ * pointers (a cudaStream_t is passed as void*).
+ */
+#ifndef NVRAR_H
+#define NVRAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NVRAR_ABI_VERSION 1
+#define NVRAR_MAX_RANKS 64
+#define NVRAR_MAX_LOCAL 32
+#define NVRAR_HANDLE_BYTES 256
+
+typedef struct nvrar_comm* nvrar_comm_t;
+
+typedef enum {
+  NVRAR_SUCCESS = 0,
+  NVRAR_ERR_INTERNAL = 1,
+  NVRAR_ERR_INVALID_ARGUMENT = 2,
+  NVRAR_ERR_INVALID_TOPOLOGY = 3,
+  NVRAR_ERR_PROTOCOL_FAULT = 4,
+  NVRAR_ERR_DEADLOCK = 5,
+  NVRAR_ERR_CUDA = 6,
+  NVRAR_ERR_NOT_CONNECTED = 7
+} nvrar_status_t;
+
+typedef enum { NVRAR_INT32 = 0, NVRAR_FLOAT32 = 1, NVRAR_BF16 = 2 } nvrar_dtype_t;
+
+typedef enum { NVRAR_SUM = 0 } nvrar_op_t;
+
+/* Communication schedule. Every schedule computes the SAME bits (the
+ * reference's reduction order for the comm's nodes x gpus_per_node); they
+ * differ only in how data moves over NVLink:
+ *   HIER    — the paper's three phases: intra-group reduce-scatter, inter-group
+ *             recursive doubling on the shard, intra-group all-gather.
+ *   TWOSHOT — flat reduce-scatter over all ranks + flat all-gather.
+ *   ONESHOT — every rank receives every input and reduces the whole vector.
+ *   AUTO    — the measured selector picks per (world, bytes). */
+typedef enum {
+  NVRAR_ALGO_AUTO = 0,
+  NVRAR_ALGO_HIER = 1,
+  NVRAR_ALGO_TWOSHOT = 2,
+  NVRAR_ALGO_ONESHOT = 3
+} nvrar_algo_t;
+
+/* Bootstrap collective supplied by the caller for nvrar_init: gather `bytes`
+ * from every rank into recv (rank-major). Return 0 on success. */
+typedef int (*nvrar_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
+
+typedef struct {
+  int world_size;
+  int rank;               /* global rank = node * gpus_per_node + local */
+  int nodes;              /* virtual nodes; power of two (nvrar.hpp:46) */
+  int gpus_per_node;
+  int device;             /* CUDA device ordinal this rank runs on */
+  size_t max_bytes;       /* largest message; sizes the symmetric staging */
+  int blocks;             /* default NvrarConfig.blocks (0 = selector) */
+  uint64_t chunk_bytes;   /* default NvrarConfig.chunk_bytes (0 = 65536) */
+  double timeout_s;       /* device watchdog (DeadlockError); 0 = 10 s */
+  nvrar_allgather_fn allgather; /* used by nvrar_init only */
+  void* allgather_ctx;
+} nvrar_init_args;
+
+typedef struct {
+  unsigned char bytes[NVRAR_HANDLE_BYTES];
+} nvrar_handle_t;
+
+/* One blocked wait recorded by the device watchdog (BlockedRank,
+ * errors.hpp:46-57). kind: 0 = FlagWait (data word), 1 = SeqWait (peer
+ * sequence/length word), 2 = length mismatch, 3 = stale/future flag. */
+typedef struct {
+  int global_rank;
+  int kind;
+  int peer_rank;
+  uint32_t expected;  /* awaited sequence number */
+  uint64_t word_index;
+  uint64_t observed;
+  int status;         /* nvrar_status_t of the fault */
+} nvrar_blocked_t;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+int nvrar_init(const nvrar_init_args* args, nvrar_comm_t* comm);
+int nvrar_comm_create(const nvrar_init_args* args, nvrar_comm_t* comm);
+int nvrar_comm_export(nvrar_comm_t comm, nvrar_handle_t* handle);
+int nvrar_comm_connect(nvrar_comm_t comm, const nvrar_handle_t* handles, int count);
+int nvrar_finalize(nvrar_comm_t comm);
+
+/* Symmetric caller buffer from the comm's own allocator (Ctx::alloc_region
+ * analogue): every rank must call it in the same order with the same size.
+ * The memory is zeroed and freed by nvrar_finalize. */
+int nvrar_alloc_symmetric(nvrar_comm_t comm, size_t bytes, void** dev_ptr);
+
+/* ---- the collective ----------------------------------------------------- */
+int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
+                    nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
+
+/* All ranks that live on ONE device (virtual ranks sharing a GPU), launched
+ * as one cooperative kernel so that ranks waiting on each other are
+ * co-resident. comms[i] runs send[i] -> recv[i]. `active_mask` bit i clear
+ * means comms[i] does not take part in this call (a stalled rank, used by
+ * the peer-only-sync fixture); pass ~0ull for all. */
+int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* send,
+                          void* const* recv, size_t count, nvrar_dtype_t dtype, nvrar_op_t op,
+                          void* stream, uint64_t active_mask);
+
+/* ---- config / introspection -------------------------------------------- */
+int nvrar_set_config(nvrar_comm_t comm, int blocks, uint64_t chunk_bytes);
+int nvrar_set_algo(nvrar_comm_t comm, nvrar_algo_t algo);
+int nvrar_set_timeout(nvrar_comm_t comm, double timeout_s);
+/* Selected schedule and CTA count for a message (what nvrar_allreduce runs). */
+int nvrar_plan(nvrar_comm_t comm, size_t count, nvrar_dtype_t dtype, int* algo, int* blocks);
+/* The same selector as a pure function (no device): every rank evaluates it
+ * identically, which is what keeps all ranks on one schedule. */
+int nvrar_plan_for(int world, int nodes, int gpus_per_node, size_t count, nvrar_dtype_t dtype,
+                   int algo_pref, int blocks_pref, int max_ctas, int* algo, int* blocks);
+/* Host-visible sequence number: synchronises with the device. */
+int nvrar_get_sequence(nvrar_comm_t comm, uint32_t* seq);
+/* Step-l exchange peers (global ranks), `steps` = log2(nodes). */
+int nvrar_get_peers(nvrar_comm_t comm, int* peers, int max_peers, int* steps);
+/* Synchronises the device and returns the sticky device status (0 = ok). */
+int nvrar_check(nvrar_comm_t comm);
+int nvrar_get_blocked(nvrar_comm_t comm, nvrar_blocked_t* out);
+const char* nvrar_last_error(nvrar_comm_t comm);
+const char* nvrar_status_string(int status);
+int nvrar_abi_version(void);
+size_t nvrar_symmetric_bytes(nvrar_comm_t comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NVRAR_H */

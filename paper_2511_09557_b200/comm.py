@@ -1,0 +1,452 @@
+"""Host-side mirror of the reference's all-reduce API over the CUDA C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/ccsim):
+
+* ``ClusterTopology`` / ``RankId``           topology.hpp:24-67
+* ``NvrarConfig``                            collectives/fused.hpp:106-116
+* ``InvalidArgumentError`` ... ``DeadlockError`` (+ ``BlockedRank``)  errors.hpp:15-85
+* ``NvrarAllreduce(comm, max_elems)`` with ``run(in, out, cfg)``,
+  ``sequence()`` and ``peers()``             collectives/nvrar.hpp:41-250
+* ``LocalGroup.run_all`` — every rank of a topology in one process (one GPU),
+  the shape of the reference's ``run_ranks`` (run.hpp:15-24); used by the
+  parity tests, as the reference's own tests drive all ranks in one process.
+
+Device tensors are torch tensors (torch is the memory/stream plumbing); all
+collective work happens in libnvrar_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib as L
+
+
+# ---- errors (errors.hpp) ------------------------------------------------------
+
+class InvalidArgumentError(ValueError):
+    """errors.hpp:15-18"""
+
+
+class InvalidTopologyError(ValueError):
+    """errors.hpp:22-25"""
+
+
+class ProtocolFaultError(RuntimeError):
+    """errors.hpp:29-43"""
+
+    def __init__(self, global_rank: int, what: str):
+        super().__init__(what if global_rank < 0 else f"rank {global_rank}: {what}")
+        self._global_rank = global_rank
+
+    def global_rank(self) -> int:
+        return self._global_rank
+
+
+@dataclass
+class BlockedRank:
+    """errors.hpp:46-57 (word_index / region describe a FlagWait)."""
+
+    class Kind(enum.IntEnum):
+        FlagWait = 0
+        SeqWait = 1
+
+    global_rank: int = -1
+    kind: "BlockedRank.Kind" = Kind.FlagWait
+    region: int = -1
+    word_index: int = 0
+    peer_rank: int = -1
+    expected: int = 0
+
+
+class DeadlockError(RuntimeError):
+    """errors.hpp:61-85 — carries the blocked set."""
+
+    def __init__(self, blocked: List[BlockedRank]):
+        self._blocked = list(blocked)
+        parts = []
+        for b in self._blocked:
+            if b.kind == BlockedRank.Kind.FlagWait:
+                parts.append(f"[rank {b.global_rank} awaits flag {b.expected} from rank "
+                             f"{b.peer_rank} word {b.word_index}]")
+            else:
+                parts.append(f"[rank {b.global_rank} awaits seq {b.expected} from rank "
+                             f"{b.peer_rank}]")
+        super().__init__(f"deadlock: {len(self._blocked)} rank(s) blocked: " + " ".join(parts))
+
+    def blocked(self) -> List[BlockedRank]:
+        return self._blocked
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(code: int, msg: str, rank: int = -1):
+    if code == L.ERR_INVALID_ARGUMENT:
+        raise InvalidArgumentError(msg)
+    if code == L.ERR_INVALID_TOPOLOGY:
+        raise InvalidTopologyError(msg)
+    if code == L.ERR_PROTOCOL_FAULT:
+        raise ProtocolFaultError(rank, msg)
+    if code == L.ERR_DEADLOCK:
+        raise DeadlockError([])
+    raise CudaError(f"nvrar error {code}: {msg}")
+
+
+# ---- topology (topology.hpp) ------------------------------------------------
+
+def is_power_of_two(v: int) -> bool:
+    return v > 0 and (v & (v - 1)) == 0
+
+
+def log2_exact(v: int) -> int:
+    lv = 0
+    while (1 << lv) < v:
+        lv += 1
+    return lv
+
+
+@dataclass(frozen=True)
+class ClusterTopology:
+    nodes: int = 1
+    gpus_per_node: int = 1
+
+    def world_size(self) -> int:
+        return self.nodes * self.gpus_per_node
+
+    def validate(self) -> None:
+        if self.nodes < 1 or self.gpus_per_node < 1:
+            raise InvalidArgumentError("topology: nodes and gpus_per_node must be >= 1")
+
+    def require_power_of_two_nodes(self, who: str) -> None:
+        self.validate()
+        if not is_power_of_two(self.nodes):
+            raise InvalidTopologyError(
+                f"{who}: node count must be a power of two, got {self.nodes}")
+
+
+@dataclass(frozen=True)
+class RankId:
+    node_rank: int = 0
+    local_rank: int = 0
+
+    def global_(self, topo: ClusterTopology) -> int:
+        return self.node_rank * topo.gpus_per_node + self.local_rank
+
+    @staticmethod
+    def from_global(g: int, topo: ClusterTopology) -> "RankId":
+        return RankId(g // topo.gpus_per_node, g % topo.gpus_per_node)
+
+    def same_node(self, other: "RankId") -> bool:
+        return self.node_rank == other.node_rank
+
+
+# ---- config (fused.hpp:106-116) ------------------------------------------------
+
+@dataclass
+class NvrarConfig:
+    """``blocks`` = CTAs per rank (the reference's independent block ranges);
+    ``chunk_bytes`` is validated like the reference's. On the GPU every thread
+    forwards its own 4-element unit as soon as it is reduced, so the chunk
+    pipeline of rd_block (nvrar.hpp:193-220) runs at unit granularity and the
+    result is, as in the reference, invariant to (blocks, chunk_bytes).
+    ``blocks = 0`` lets the selector choose."""
+
+    blocks: int = 0
+    chunk_bytes: int = 65536
+
+    def validate(self) -> None:
+        if self.blocks < 0:
+            raise InvalidArgumentError("nvrar config: blocks must be >= 1")
+        if self.chunk_bytes < 8 or self.chunk_bytes % 8 != 0:
+            raise InvalidArgumentError("nvrar config: chunk_bytes must be a multiple of 8, >= 8")
+
+
+_DTYPES = {torch.float32: L.FLOAT32, torch.bfloat16: L.BF16, torch.int32: L.INT32}
+_ALGOS = {"auto": L.ALGO_AUTO, "hier": L.ALGO_HIER, "twoshot": L.ALGO_TWOSHOT,
+          "oneshot": L.ALGO_ONESHOT}
+
+
+def dtype_code(t: torch.dtype) -> int:
+    try:
+        return _DTYPES[t]
+    except KeyError:
+        raise InvalidArgumentError(f"unsupported dtype {t} (int32, float32, bfloat16)") from None
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# ---- communicator --------------------------------------------------------------
+
+class Communicator:
+    """One rank's NVRAR communicator (nvrar_comm_t)."""
+
+    def __init__(self, topo: ClusterTopology, rank: int, device: int, max_bytes: int,
+                 timeout_s: float = 10.0, blocks: int = 0, chunk_bytes: int = 65536):
+        topo.require_power_of_two_nodes("nvrar")
+        self.topo = topo
+        self.rank = rank
+        self.device = device
+        self.max_bytes = max_bytes
+        self._lib = L.load()
+        args = L.InitArgs(world_size=topo.world_size(), rank=rank, nodes=topo.nodes,
+                          gpus_per_node=topo.gpus_per_node, device=device,
+                          max_bytes=max_bytes, blocks=blocks, chunk_bytes=chunk_bytes,
+                          timeout_s=timeout_s)
+        h = ctypes.c_void_p()
+        rc = self._lib.nvrar_comm_create(ctypes.byref(args), ctypes.byref(h))
+        if rc != 0:
+            _raise(rc, self._lib.nvrar_last_error(None).decode(), rank)
+        self._h = h
+        self.connected = False
+
+    # -- bootstrap --------------------------------------------------------------
+    def export(self) -> bytes:
+        hd = L.Handle()
+        self._check(self._lib.nvrar_comm_export(self._h, ctypes.byref(hd)))
+        return bytes(hd.bytes)
+
+    def connect(self, handles: Sequence[bytes]) -> None:
+        arr = (L.Handle * len(handles))()
+        for i, b in enumerate(handles):
+            ctypes.memmove(arr[i].bytes, b, L.HANDLE_BYTES)
+        self._check(self._lib.nvrar_comm_connect(self._h, arr, len(handles)))
+        self.connected = True
+
+    @classmethod
+    def from_process_group(cls, topo: ClusterTopology, max_bytes: int, device: Optional[int] = None,
+                           group=None, **kw) -> "Communicator":
+        """One process per GPU: exchange IPC handles over torch.distributed."""
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        if device is None:
+            device = torch.cuda.current_device()
+        comm = cls(topo, rank, device, max_bytes, **kw)
+        mine = comm.export()
+        allh: List[Optional[bytes]] = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, mine, group=group)
+        comm.connect(allh)  # type: ignore[arg-type]
+        return comm
+
+    # -- knobs / introspection --------------------------------------------------
+    def set_config(self, cfg: NvrarConfig) -> None:
+        cfg.validate()
+        self._check(self._lib.nvrar_set_config(self._h, cfg.blocks, cfg.chunk_bytes))
+
+    def set_algo(self, algo: str) -> None:
+        self._check(self._lib.nvrar_set_algo(self._h, _ALGOS[algo]))
+
+    def set_timeout(self, seconds: float) -> None:
+        self._check(self._lib.nvrar_set_timeout(self._h, seconds))
+
+    def plan(self, count: int, dtype: torch.dtype):
+        a, b = ctypes.c_int(), ctypes.c_int()
+        self._check(self._lib.nvrar_plan(self._h, count, dtype_code(dtype), ctypes.byref(a),
+                                         ctypes.byref(b)))
+        return L.ALGO_NAMES[a.value], b.value
+
+    def sequence(self) -> int:
+        s = ctypes.c_uint32()
+        self._check(self._lib.nvrar_get_sequence(self._h, ctypes.byref(s)))
+        return s.value
+
+    def peers(self) -> List[RankId]:
+        arr = (ctypes.c_int * 8)()
+        steps = ctypes.c_int()
+        self._check(self._lib.nvrar_get_peers(self._h, arr, 8, ctypes.byref(steps)))
+        return [RankId.from_global(arr[i], self.topo) for i in range(steps.value)]
+
+    def blocked(self) -> L.Blocked:
+        b = L.Blocked()
+        self._check(self._lib.nvrar_get_blocked(self._h, ctypes.byref(b)))
+        return b
+
+    def check_status(self) -> int:
+        """Synchronise and return the sticky device status (0 = ok)."""
+        return self._lib.nvrar_check(self._h)
+
+    def check(self) -> None:
+        rc = self.check_status()
+        if rc == L.ERR_DEADLOCK:
+            raise DeadlockError([_blocked_rank(self.blocked())])
+        if rc:
+            _raise(rc, self.last_error(), self.rank)
+
+    def last_error(self) -> str:
+        return self._lib.nvrar_last_error(self._h).decode()
+
+    def symmetric_bytes(self) -> int:
+        return int(self._lib.nvrar_symmetric_bytes(self._h))
+
+    # -- the collective -------------------------------------------------------------
+    def allreduce(self, send: torch.Tensor, recv: torch.Tensor,
+                  stream: Optional[torch.cuda.Stream] = None) -> None:
+        """nvrar_allreduce(send, recv, count, dtype, SUM, stream) — asynchronous."""
+        _check_pair(send, recv)
+        rc = self._lib.nvrar_allreduce(self._h, send.data_ptr(), recv.data_ptr(), send.numel(),
+                                       dtype_code(send.dtype), L.SUM, _stream_ptr(stream))
+        if rc:
+            _raise(rc, self.last_error(), self.rank)
+
+    def allreduce_raw(self, send_ptr: int, recv_ptr: int, count: int, dtype: int,
+                      stream_ptr: int) -> None:
+        rc = self._lib.nvrar_allreduce(self._h, send_ptr, recv_ptr, count, dtype, L.SUM,
+                                       stream_ptr)
+        if rc:
+            _raise(rc, self.last_error(), self.rank)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.nvrar_finalize(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int) -> None:
+        if rc:
+            _raise(rc, self.last_error(), self.rank)
+
+
+def _blocked_rank(b: L.Blocked) -> BlockedRank:
+    return BlockedRank(global_rank=b.global_rank,
+                       kind=BlockedRank.Kind.SeqWait if b.kind == 1 else BlockedRank.Kind.FlagWait,
+                       word_index=b.word_index, peer_rank=b.peer_rank, expected=b.expected)
+
+
+def _check_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
+    if send.numel() != recv.numel():
+        raise InvalidArgumentError("nvrar: input and output lengths differ")
+    if send.dtype != recv.dtype:
+        raise InvalidArgumentError("nvrar: input and output dtypes differ")
+    if not (send.is_cuda and recv.is_cuda):
+        raise InvalidArgumentError("nvrar: buffers must be CUDA tensors")
+    if not (send.is_contiguous() and recv.is_contiguous()):
+        raise InvalidArgumentError("nvrar: buffers must be contiguous")
+
+
+# ---- the reference-shaped collective ------------------------------------------------
+
+class NvrarAllreduce:
+    """Per-rank NVRAR state, as ``ccsim::NvrarAllreduce<T>`` (nvrar.hpp:41-250).
+
+    ``comm`` owns the symmetric staging sized for ``max_elems`` elements of the
+    widest use; ``run`` launches the persistent kernel on the current stream.
+    """
+
+    def __init__(self, comm: Communicator, max_elems: int):
+        self.comm = comm
+        self.max_elems = max_elems
+
+    def sequence(self) -> int:
+        return self.comm.sequence()
+
+    def peers(self) -> List[RankId]:
+        return self.comm.peers()
+
+    def run(self, inp: torch.Tensor, out: torch.Tensor, cfg: NvrarConfig = NvrarConfig(),
+            stream: Optional[torch.cuda.Stream] = None, sync: bool = False) -> None:
+        cfg.validate()
+        if inp.numel() != out.numel():
+            raise InvalidArgumentError("nvrar: input and output lengths differ")
+        if inp.numel() > self.max_elems:
+            raise InvalidArgumentError("nvrar: vector longer than the preallocated maximum")
+        self.comm.set_config(cfg)
+        self.comm.allreduce(inp, out, stream)
+        if sync:
+            self.comm.check()
+
+
+class LocalGroup:
+    """Every rank of ``topo`` as a virtual rank on ONE device, each with its own
+    communicator and symmetric region; one cooperative launch runs them all.
+    This is the all-ranks-in-one-process shape of the reference's run_ranks
+    (run.hpp:15-24), on a GPU."""
+
+    def __init__(self, topo: ClusterTopology, max_bytes: int, device: int = 0,
+                 timeout_s: float = 10.0):
+        topo.require_power_of_two_nodes("nvrar")
+        p = topo.world_size()
+        if p > L.MAX_LOCAL:
+            raise InvalidArgumentError(f"at most {L.MAX_LOCAL} virtual ranks per device")
+        self.topo = topo
+        self.device = device
+        self.comms = [Communicator(topo, r, device, max_bytes, timeout_s=timeout_s)
+                      for r in range(p)]
+        handles = [c.export() for c in self.comms]
+        for c in self.comms:
+            c.connect(handles)
+        self._lib = L.load()
+        self._arr = (ctypes.c_void_p * p)(*[c._h.value for c in self.comms])
+
+    def set_config(self, cfg: NvrarConfig) -> None:
+        for c in self.comms:
+            c.set_config(cfg)
+
+    def set_algo(self, algo: str) -> None:
+        for c in self.comms:
+            c.set_algo(algo)
+
+    def set_timeout(self, s: float) -> None:
+        for c in self.comms:
+            c.set_timeout(s)
+
+    def launch(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
+               active: Optional[Sequence[int]] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> None:
+        p = self.topo.world_size()
+        if len(inputs) != p or len(outputs) != p:
+            raise InvalidArgumentError("one input and one output per rank")
+        for a, b in zip(inputs, outputs):
+            _check_pair(a, b)
+        n = inputs[0].numel()
+        dt = dtype_code(inputs[0].dtype)
+        send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
+        recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])
+        mask = (1 << 64) - 1 if active is None else sum(1 << r for r in active)
+        rc = self._lib.nvrar_allreduce_local(self._arr, p, send, recv, n, dt, L.SUM,
+                                             _stream_ptr(stream), mask)
+        if rc:
+            _raise(rc, self.comms[0].last_error())
+
+    def check(self) -> None:
+        """Synchronise; raise the reference's exception for the first fault.
+        A deadlock reports the blocked set over all ranks (errors.hpp:61-85)."""
+        torch.cuda.synchronize(self.device)
+        codes = [c.check_status() for c in self.comms]
+        if any(code == L.ERR_DEADLOCK for code in codes) and not any(
+                code == L.ERR_PROTOCOL_FAULT for code in codes):
+            blocked = [_blocked_rank(c.blocked()) for c, code in zip(self.comms, codes)
+                       if code == L.ERR_DEADLOCK]
+            raise DeadlockError(sorted(blocked, key=lambda b: b.global_rank))
+        for c, code in zip(self.comms, codes):
+            if code:
+                _raise(code, c.last_error(), c.rank)
+
+    def run_all(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
+                cfg: Optional[NvrarConfig] = None, active: Optional[Sequence[int]] = None,
+                check: bool = True) -> None:
+        if cfg is not None:
+            self.set_config(cfg)
+        self.launch(inputs, outputs, active)
+        if check:
+            self.check()
+
+    def sequences(self) -> List[int]:
+        return [c.sequence() for c in self.comms]
+
+    def close(self) -> None:
+        for c in self.comms:
+            c.close()

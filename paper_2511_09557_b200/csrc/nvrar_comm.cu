@@ -1,0 +1,618 @@
+// Host runtime behind include/nvrar.h: communicator lifecycle, symmetric
+// region + CUDA IPC peer mapping, schedule selection, launches and fault
+// reporting. One communicator per rank (per process, or several virtual ranks
+// per device for the all-ranks-in-one-launch mode).
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/nvrar.h"
+#include "nvrar_device.cuh"
+
+namespace nvrar {
+using KernelFn = void (*)(LaunchParams);
+KernelFn select_kernel(int dtype, bool flat, int nodes);
+KernelFn bump_kernel();
+int flat_max_gpus(int nodes);
+}  // namespace nvrar
+
+using namespace nvrar;
+
+namespace {
+
+constexpr uint32_t kMagic = 0x4E565241u;  // "NVRA"
+constexpr uint64_t kOneshotMaxBytes = 1ull << 20;
+
+struct HandleBlob {
+  uint32_t magic;
+  uint32_t version;
+  int32_t pid;
+  int32_t device;
+  int32_t rank, world, nodes, gpus;
+  uint64_t max_bytes;
+  uint64_t region_ptr;
+  uint64_t region_bytes;
+  uint64_t layout_bytes;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(HandleBlob) <= NVRAR_HANDLE_BYTES, "handle too large");
+
+std::string g_global_error;
+
+int log2_exact(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return l;
+}
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+size_t dtype_bytes(int dt) { return dt == NVRAR_BF16 ? 2 : 4; }
+
+uint64_t units_for(uint64_t elems) { return (elems + kUnit - 1) / kUnit + 1; }
+
+}  // namespace
+
+struct nvrar_comm {
+  int world = 0, rank = 0, nodes = 1, gpus = 1, device = 0, steps = 0;
+  size_t max_bytes = 0;
+  Layout lay{};
+  uint8_t* region = nullptr;
+  RankState* state = nullptr;
+  RankDesc* d_desc = nullptr;
+  RankDesc h_desc{};
+  std::vector<uint8_t*> opened;  // IPC mappings to close
+  std::vector<void*> sym_allocs;
+  int blocks = 0;
+  uint64_t chunk_bytes = 65536;
+  int algo = NVRAR_ALGO_AUTO;
+  double timeout_s = 10.0;
+  bool connected = false;
+  int sticky = 0;
+  std::string last_error;
+  int max_ctas = 148;  // co-resident CTAs of one kernel on this device
+};
+
+namespace {
+
+int fail(nvrar_comm* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->last_error = buf;
+  } else {
+    g_global_error = buf;
+  }
+  return code;
+}
+
+#define CUDA_TRY(c, expr)                                                         \
+  do {                                                                            \
+    cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      return fail((c), NVRAR_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                            \
+    }                                                                             \
+  } while (0)
+
+Layout make_layout(int world, int nodes, int gpus, size_t max_bytes) {
+  // Sized for the worst dtype (bf16: most elements per byte) and every schedule.
+  const uint64_t max_elems = std::max<uint64_t>(max_bytes / 2, 4);
+  const uint64_t ug = units_for((max_elems + gpus - 1) / gpus);
+  const uint64_t up = units_for((max_elems + world - 1) / world + 3);
+  const uint64_t u1 = units_for(std::min<uint64_t>(max_elems, kOneshotMaxBytes / 2));
+  const int steps = log2_exact(nodes);
+  Layout l{};
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) {
+    const uint64_t o = off;
+    off += (bytes + 255) & ~255ull;
+    return o;
+  };
+  l.ctrl_off = take(sizeof(uint64_t) * kMaxRanks);
+  // 4 LL words (32 B) per unit; 32-unit groups so round up to 32 units.
+  auto slot_words = [](uint64_t units) { return ((units + 31) & ~31ull) * 4; };
+  l.a_src = slot_words(std::max({gpus > 1 ? ug : 0, up, u1}));
+  l.a_off = take(2ull * world * l.a_src * 8);
+  l.b_src = slot_words(std::max(gpus > 1 ? ug : 0, up));
+  l.b_off = take(2ull * world * l.b_src * 8);
+  l.c_step = slot_words(ug);
+  l.c_off = take(2ull * std::max(steps, 1) * l.c_step * 8);
+  l.bytes = off;
+  return l;
+}
+
+int validate_args(const nvrar_init_args* a) {
+  if (!a) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null init args");
+  if (a->nodes < 1 || a->gpus_per_node < 1) {
+    return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT,
+                "topology: nodes and gpus_per_node must be >= 1");
+  }
+  if (!is_pow2(a->nodes)) {
+    return fail(nullptr, NVRAR_ERR_INVALID_TOPOLOGY,
+                "nvrar: node count must be a power of two, got %d", a->nodes);
+  }
+  if (a->nodes > 8 || a->gpus_per_node > 8) {
+    return fail(nullptr, NVRAR_ERR_INVALID_TOPOLOGY,
+                "nvrar_b200: supports nodes <= 8 and gpus_per_node <= 8 (got %dx%d)",
+                a->nodes, a->gpus_per_node);
+  }
+  if (a->world_size != a->nodes * a->gpus_per_node) {
+    return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "world_size %d != nodes*gpus %d",
+                a->world_size, a->nodes * a->gpus_per_node);
+  }
+  if (a->rank < 0 || a->rank >= a->world_size) {
+    return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "rank %d out of range", a->rank);
+  }
+  if (a->blocks < 0) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "blocks must be >= 0");
+  if (a->chunk_bytes != 0 && (a->chunk_bytes < 8 || a->chunk_bytes % 8 != 0)) {
+    return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT,
+                "nvrar config: chunk_bytes must be a multiple of 8, >= 8");
+  }
+  return NVRAR_SUCCESS;
+}
+
+// Schedule + CTA count for one call (nvrar_plan / nvrar_plan_for). A pure
+// function of its arguments, so every rank picks the same schedule. The
+// default policy is the measured one from the B200 sweep (DESIGN.md,
+// "selector"); user overrides (algo / blocks) win.
+void plan_shape(int world, int nodes, int gpus, int algo_pref, int blocks_pref, int max_ctas,
+                uint64_t count, int dtype, int* algo, int* blocks) {
+  const uint64_t bytes = count * dtype_bytes(dtype);
+  const bool flat_ok = gpus <= flat_max_gpus(nodes) && world <= 16;
+  int a = algo_pref;
+  if (a == NVRAR_ALGO_AUTO) {
+    if (!flat_ok) {
+      a = NVRAR_ALGO_HIER;
+    } else if (world == 1 || bytes <= 64 * 1024) {
+      a = NVRAR_ALGO_ONESHOT;
+    } else {
+      a = NVRAR_ALGO_TWOSHOT;
+    }
+  }
+  if ((a == NVRAR_ALGO_TWOSHOT || a == NVRAR_ALGO_ONESHOT) && !flat_ok) a = NVRAR_ALGO_HIER;
+  if (a == NVRAR_ALGO_ONESHOT && bytes > kOneshotMaxBytes) a = NVRAR_ALGO_TWOSHOT;
+  uint64_t units;
+  if (a == NVRAR_ALGO_HIER) {
+    units = (((count + gpus - 1) / gpus) + 3) / 4;
+  } else if (a == NVRAR_ALGO_ONESHOT) {
+    units = (count + 3) / 4;
+  } else {
+    units = ((count + world - 1) / world + 3) / 4;
+  }
+  int b = blocks_pref;
+  if (b <= 0) {
+    // one unit per thread where possible, at least a few CTAs for NVLink injection
+    const uint64_t want = (units + kThreads - 1) / kThreads;
+    b = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(want, 4), 128));
+  }
+  b = std::max(1, std::min(b, max_ctas));
+  *algo = a;
+  *blocks = b;
+}
+
+void plan(const nvrar_comm* c, uint64_t count, int dtype, int* algo, int* blocks) {
+  plan_shape(c->world, c->nodes, c->gpus, c->algo, c->blocks, c->max_ctas, count, dtype, algo,
+             blocks);
+}
+
+int check_sticky(nvrar_comm* c) {
+  if (c->sticky) return c->sticky;
+  return NVRAR_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nvrar_abi_version(void) { return NVRAR_ABI_VERSION; }
+
+const char* nvrar_status_string(int s) {
+  switch (s) {
+    case NVRAR_SUCCESS: return "success";
+    case NVRAR_ERR_INTERNAL: return "internal error";
+    case NVRAR_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case NVRAR_ERR_INVALID_TOPOLOGY: return "invalid topology";
+    case NVRAR_ERR_PROTOCOL_FAULT: return "protocol fault";
+    case NVRAR_ERR_DEADLOCK: return "deadlock";
+    case NVRAR_ERR_CUDA: return "cuda error";
+    case NVRAR_ERR_NOT_CONNECTED: return "not connected";
+    default: return "unknown";
+  }
+}
+
+const char* nvrar_last_error(nvrar_comm_t comm) {
+  return comm ? comm->last_error.c_str() : g_global_error.c_str();
+}
+
+int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
+  if (!out) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm out");
+  *out = nullptr;
+  int rc = validate_args(a);
+  if (rc) return rc;
+  auto* c = new nvrar_comm();
+  c->world = a->world_size;
+  c->rank = a->rank;
+  c->nodes = a->nodes;
+  c->gpus = a->gpus_per_node;
+  c->device = a->device;
+  c->steps = log2_exact(a->nodes);
+  c->max_bytes = std::max<size_t>(a->max_bytes, 16);
+  c->blocks = a->blocks;
+  c->chunk_bytes = a->chunk_bytes ? a->chunk_bytes : 65536;
+  c->timeout_s = a->timeout_s > 0 ? a->timeout_s : 10.0;
+  c->lay = make_layout(c->world, c->nodes, c->gpus, c->max_bytes);
+
+  auto cleanup = [&](int code) {
+    if (c->region) cudaFree(c->region);
+    if (c->state) cudaFree(c->state);
+    if (c->d_desc) cudaFree(c->d_desc);
+    g_global_error = c->last_error;
+    delete c;
+    return code;
+  };
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) {
+    fail(c, NVRAR_ERR_CUDA, "cudaSetDevice(%d): %s", c->device, cudaGetErrorString(e));
+    return cleanup(NVRAR_ERR_CUDA);
+  }
+  if ((e = cudaMalloc(&c->region, c->lay.bytes)) != cudaSuccess ||
+      (e = cudaMemset(c->region, 0, c->lay.bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&c->state, sizeof(RankState))) != cudaSuccess ||
+      (e = cudaMemset(c->state, 0, sizeof(RankState))) != cudaSuccess ||
+      (e = cudaMalloc(&c->d_desc, sizeof(RankDesc))) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    fail(c, NVRAR_ERR_CUDA, "allocating %llu B symmetric region: %s",
+         static_cast<unsigned long long>(c->lay.bytes), cudaGetErrorString(e));
+    return cleanup(NVRAR_ERR_CUDA);
+  }
+  int sms = 148, occ = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  for (int flat = 0; flat < 2; ++flat) {
+    for (int dt = 0; dt < 3; ++dt) {
+      int o = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &o, reinterpret_cast<const void*>(select_kernel(dt, flat, c->nodes)), kThreads,
+              0) == cudaSuccess &&
+          o > 0) {
+        occ = flat + dt == 0 ? o : std::min(occ, o);
+      }
+    }
+  }
+  c->max_ctas = std::max(1, sms * std::max(occ, 1));
+  c->h_desc = RankDesc{};
+  c->h_desc.state = c->state;
+  c->h_desc.lay = c->lay;
+  c->h_desc.rank = c->rank;
+  c->h_desc.world = c->world;
+  c->h_desc.nodes = c->nodes;
+  c->h_desc.gpus = c->gpus;
+  c->h_desc.steps = c->steps;
+  c->h_desc.node = c->rank / c->gpus;
+  c->h_desc.local = c->rank % c->gpus;
+  c->h_desc.timeout_ns = static_cast<uint64_t>(c->timeout_s * 1e9);
+  c->h_desc.base[c->rank] = c->region;
+  *out = c;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_comm_export(nvrar_comm_t c, nvrar_handle_t* h) {
+  if (!c || !h) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  HandleBlob b{};
+  b.magic = kMagic;
+  b.version = NVRAR_ABI_VERSION;
+  b.pid = static_cast<int32_t>(getpid());
+  b.device = c->device;
+  b.rank = c->rank;
+  b.world = c->world;
+  b.nodes = c->nodes;
+  b.gpus = c->gpus;
+  b.max_bytes = c->max_bytes;
+  b.region_ptr = reinterpret_cast<uint64_t>(c->region);
+  b.region_bytes = c->lay.bytes;
+  b.layout_bytes = c->lay.bytes;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaIpcGetMemHandle(&b.ipc, c->region));
+  std::memset(h->bytes, 0, sizeof(h->bytes));
+  std::memcpy(h->bytes, &b, sizeof(b));
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_comm_connect(nvrar_comm_t c, const nvrar_handle_t* hs, int count) {
+  if (!c || !hs) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  if (count != c->world) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "expected %d handles, got %d", c->world, count);
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int32_t mypid = static_cast<int32_t>(getpid());
+  for (int r = 0; r < count; ++r) {
+    HandleBlob b;
+    std::memcpy(&b, hs[r].bytes, sizeof(b));
+    if (b.magic != kMagic || b.version != NVRAR_ABI_VERSION) {
+      return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "handle %d: bad magic/version", r);
+    }
+    if (b.rank != r || b.world != c->world || b.nodes != c->nodes || b.gpus != c->gpus ||
+        b.max_bytes != c->max_bytes || b.layout_bytes != c->lay.bytes) {
+      return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                  "handle %d: peer comm shape differs (rank %d world %d %dx%d max %llu)", r,
+                  b.rank, b.world, b.nodes, b.gpus,
+                  static_cast<unsigned long long>(b.max_bytes));
+    }
+    if (r == c->rank) continue;
+    if (b.pid == mypid) {
+      if (b.device != c->device) {
+        int can = 0;
+        CUDA_TRY(c, cudaDeviceCanAccessPeer(&can, c->device, b.device));
+        if (!can) {
+          return fail(c, NVRAR_ERR_CUDA, "device %d cannot access peer %d", c->device, b.device);
+        }
+        cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          return fail(c, NVRAR_ERR_CUDA, "enable peer access: %s", cudaGetErrorString(e));
+        }
+        cudaGetLastError();
+      }
+      c->h_desc.base[r] = reinterpret_cast<uint8_t*>(b.region_ptr);
+    } else {
+      void* p = nullptr;
+      CUDA_TRY(c, cudaIpcOpenMemHandle(&p, b.ipc, cudaIpcMemLazyEnablePeerAccess));
+      c->h_desc.base[r] = static_cast<uint8_t*>(p);
+      c->opened.push_back(static_cast<uint8_t*>(p));
+    }
+  }
+  CUDA_TRY(c, cudaMemcpy(c->d_desc, &c->h_desc, sizeof(RankDesc), cudaMemcpyHostToDevice));
+  c->connected = true;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_init(const nvrar_init_args* a, nvrar_comm_t* out) {
+  int rc = validate_args(a);
+  if (rc) return rc;
+  if (!a->allgather) {
+    return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "nvrar_init needs an allgather callback");
+  }
+  nvrar_comm_t c = nullptr;
+  rc = nvrar_comm_create(a, &c);
+  if (rc) return rc;
+  nvrar_handle_t mine;
+  rc = nvrar_comm_export(c, &mine);
+  if (rc) {
+    g_global_error = c->last_error;
+    nvrar_finalize(c);
+    return rc;
+  }
+  std::vector<nvrar_handle_t> all(a->world_size);
+  if (a->allgather(a->allgather_ctx, &mine, all.data(), sizeof(nvrar_handle_t)) != 0) {
+    nvrar_finalize(c);
+    return fail(nullptr, NVRAR_ERR_INTERNAL, "bootstrap allgather failed");
+  }
+  rc = nvrar_comm_connect(c, all.data(), a->world_size);
+  if (rc) {
+    g_global_error = c->last_error;
+    nvrar_finalize(c);
+    return rc;
+  }
+  *out = c;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_finalize(nvrar_comm_t c) {
+  if (!c) return NVRAR_SUCCESS;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (auto* p : c->sym_allocs) cudaFree(p);
+  if (c->region) cudaFree(c->region);
+  if (c->state) cudaFree(c->state);
+  if (c->d_desc) cudaFree(c->d_desc);
+  delete c;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_alloc_symmetric(nvrar_comm_t c, size_t bytes, void** p) {
+  if (!c || !p) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  void* q = nullptr;
+  CUDA_TRY(c, cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+  CUDA_TRY(c, cudaMemset(q, 0, std::max<size_t>(bytes, 16)));
+  c->sym_allocs.push_back(q);
+  *p = q;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_set_config(nvrar_comm_t c, int blocks, uint64_t chunk_bytes) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  // NvrarConfig::validate (fused.hpp:110-115); blocks == 0 selects automatically.
+  if (blocks < 0) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "nvrar config: blocks must be >= 1");
+  if (chunk_bytes < 8 || chunk_bytes % 8 != 0) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                "nvrar config: chunk_bytes must be a multiple of 8, >= 8");
+  }
+  c->blocks = blocks;
+  c->chunk_bytes = chunk_bytes;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_set_algo(nvrar_comm_t c, nvrar_algo_t algo) {
+  if (!c || algo < NVRAR_ALGO_AUTO || algo > NVRAR_ALGO_ONESHOT) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad algo");
+  }
+  if ((algo == NVRAR_ALGO_TWOSHOT || algo == NVRAR_ALGO_ONESHOT) &&
+      (c->gpus > flat_max_gpus(c->nodes) || c->world > 16)) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "flat schedules support at most %d gpus per node at %d nodes",
+                flat_max_gpus(c->nodes), c->nodes);
+  }
+  c->algo = algo;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_set_timeout(nvrar_comm_t c, double timeout_s) {
+  if (!c || !(timeout_s > 0)) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad timeout");
+  c->timeout_s = timeout_s;
+  c->h_desc.timeout_ns = static_cast<uint64_t>(timeout_s * 1e9);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpy(c->d_desc, &c->h_desc, sizeof(RankDesc), cudaMemcpyHostToDevice));
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_plan(nvrar_comm_t c, size_t count, nvrar_dtype_t dtype, int* algo, int* blocks) {
+  if (!c || !algo || !blocks) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  plan(c, count, dtype, algo, blocks);
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_plan_for(int world, int nodes, int gpus, size_t count, nvrar_dtype_t dtype,
+                   int algo_pref, int blocks_pref, int max_ctas, int* algo, int* blocks) {
+  if (!algo || !blocks || world != nodes * gpus || !is_pow2(nodes) || max_ctas < 1) {
+    return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad plan query");
+  }
+  plan_shape(world, nodes, gpus, algo_pref, blocks_pref, max_ctas, count, dtype, algo, blocks);
+  return NVRAR_SUCCESS;
+}
+
+size_t nvrar_symmetric_bytes(nvrar_comm_t c) { return c ? c->lay.bytes : 0; }
+
+int nvrar_get_peers(nvrar_comm_t c, int* peers, int max_peers, int* steps) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  if (steps) *steps = c->steps;
+  const int node = c->rank / c->gpus, local = c->rank % c->gpus;
+  for (int l = 0; l < c->steps && l < max_peers; ++l) {
+    peers[l] = ((node ^ (1 << l)) * c->gpus) + local;  // nvrar.hpp:72-75
+  }
+  return NVRAR_SUCCESS;
+}
+
+static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void* const* recv,
+                  size_t count, int dtype, int op, void* stream, uint64_t mask, bool local_group) {
+  nvrar_comm* c0 = comms[0];
+  if (op != NVRAR_SUM) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "only SUM is supported");
+  if (dtype < NVRAR_INT32 || dtype > NVRAR_BF16) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  }
+  LaunchParams lp{};
+  int nl = 0;
+  for (int i = 0; i < ncomms; ++i) {
+    nvrar_comm* c = comms[i];
+    if (!c) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "null comm %d", i);
+    if (!c->connected) return fail(c, NVRAR_ERR_NOT_CONNECTED, "comm not connected");
+    if (c->device != c0->device || c->nodes != c0->nodes || c->gpus != c0->gpus) {
+      return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "comms differ in device or topology");
+    }
+    if (int s = check_sticky(c)) return fail(c, s, "comm is in a failed state: %s", c->last_error.c_str());
+    if (count * dtype_bytes(dtype) > c->max_bytes) {
+      return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                  "nvrar: vector longer than the preallocated maximum (%zu B > %zu B)",
+                  count * dtype_bytes(dtype), c->max_bytes);
+    }
+    if (count > 0 && (!send[i] || !recv[i])) {
+      return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null buffer");
+    }
+    if (!((mask >> i) & 1ull)) continue;
+    lp.desc[nl] = c->d_desc;
+    lp.send[nl] = send[i];
+    lp.recv[nl] = recv[i];
+    ++nl;
+  }
+  if (nl == 0) return NVRAR_SUCCESS;
+  lp.nlocal = nl;
+  lp.count = count;
+  CUDA_TRY(c0, cudaSetDevice(c0->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (count == 0) {
+    // n == 0 still consumes a sequence number (nvrar.hpp:93-96).
+    bump_kernel()<<<dim3(1, nl), 32, 0, s>>>(lp);
+    CUDA_TRY(c0, cudaGetLastError());
+    return NVRAR_SUCCESS;
+  }
+  int algo = 0, blocks = 1;
+  plan(c0, count, dtype, &algo, &blocks);
+  if (local_group) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
+  KernelFn k = select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes);
+  if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
+  dim3 grid(blocks, nl), block(kThreads);
+  if (local_group && nl > 1) {
+    void* args[] = {&lp};
+    CUDA_TRY(c0, cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), grid, block, args,
+                                             0, s));
+  } else {
+    k<<<grid, block, 0, s>>>(lp);
+    CUDA_TRY(c0, cudaGetLastError());
+  }
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
+                    nvrar_dtype_t dtype, nvrar_op_t op, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  const void* s[1] = {send};
+  void* r[1] = {recv};
+  return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false);
+}
+
+int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* send,
+                          void* const* recv, size_t count, nvrar_dtype_t dtype, nvrar_op_t op,
+                          void* stream, uint64_t active_mask) {
+  if (!comms || ncomms < 1 || ncomms > NVRAR_MAX_LOCAL || !send || !recv) {
+    return fail(comms ? comms[0] : nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad local group");
+  }
+  return launch(comms, ncomms, send, recv, count, dtype, op, stream, active_mask, true);
+}
+
+int nvrar_get_sequence(nvrar_comm_t c, uint32_t* seq) {
+  if (!c || !seq) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  RankState st;
+  CUDA_TRY(c, cudaMemcpy(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
+  *seq = st.seq;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_get_blocked(nvrar_comm_t c, nvrar_blocked_t* out) {
+  if (!c || !out) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  RankState st;
+  CUDA_TRY(c, cudaMemcpy(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
+  out->global_rank = c->rank;
+  out->kind = st.err.kind;
+  out->peer_rank = st.err.peer;
+  out->expected = st.err.expected;
+  out->word_index = st.err.word;
+  out->observed = st.err.observed;
+  out->status = static_cast<int>(st.err.code);
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_check(nvrar_comm_t c) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  if (c->sticky) return c->sticky;
+  nvrar_blocked_t b;
+  int rc = nvrar_get_blocked(c, &b);
+  if (rc) return rc;
+  if (b.status == 0) return NVRAR_SUCCESS;
+  c->sticky = b.status;
+  static const char* kinds[] = {"flag", "seq", "length", "stale flag"};
+  const char* kind = (b.kind >= 0 && b.kind < 4) ? kinds[b.kind] : "?";
+  if (b.status == NVRAR_ERR_DEADLOCK) {
+    fail(c, b.status, "deadlock: rank %d awaits %s %u from rank %d (word %llu, saw 0x%llx)",
+         c->rank, kind, b.expected, b.peer_rank, static_cast<unsigned long long>(b.word_index),
+         static_cast<unsigned long long>(b.observed));
+  } else {
+    fail(c, b.status, "rank %d: protocol fault (%s) with rank %d at call %u (saw 0x%llx)",
+         c->rank, kind, b.peer_rank, b.expected, static_cast<unsigned long long>(b.observed));
+  }
+  return b.status;
+}
+
+}  // extern "C"

@@ -1,0 +1,505 @@
+// B200 (sm_100a) kernels of the NVRAR all-reduce.
+//
+// One persistent launch per call runs every phase of the schedule; no host
+// round trip, no NCCL. Two kernel families compute the SAME bits — the
+// reference's reduction order for hierarchy nodes x gpus_per_node:
+//
+//   element e, shard S = ceil(n/G), c = e / S:
+//     node partial = x[(c+1)%G] + x[(c+2)%G] + ... + x[c]   (ring_schedule.hpp:12-15,
+//                                                             oracles.hpp:49-61)
+//     result       = pairwise tree over nodes in node order  (nvrar.hpp:207-219;
+//                    i.e. v = partner + own per XOR step       oracles.hpp:122-130)
+//
+// hier_kernel — the paper's three phases (nvrar.hpp:84-129):
+//   1. intra-group reduce-scatter: every rank pushes chunk c of its input to
+//      group member c over NVLink (LL words); member c folds its chunk in the
+//      pinned order with its own copy last;
+//   2. inter-group recursive doubling on the shard (nvrar.hpp:197-220): per
+//      unit, the running fp32/int32 partial goes to the XOR peer's per-step
+//      receive slot, the partner's arrives in ours, v = partner + own, and the
+//      unit is forwarded to the next step at once (the reference's chunk
+//      pipeline at the granularity of one thread's unit);
+//   3. intra-group all-gather fused with the final cast (fp32 -> bf16 RNE):
+//      the finished shard is written to the caller's output and pushed to the
+//      group members.
+//   Before the first inter-group send each rank publishes (seq<<32 | len) to
+//   its log2(N) XOR peers and waits for theirs — the reference's peer-only
+//   sync with its length check (nvrar.hpp:163-171, ring.hpp:86-98).
+//
+// flat_kernel — the same order on a flat schedule (B200-first: every peer is
+//   one NVSwitch hop away, so the hierarchy only has to fix the ORDER):
+//   two-shot = flat reduce-scatter (rank p owns elements [p*SP, (p+1)*SP)) +
+//   flat all-gather; one-shot = every rank receives every input.
+//
+// Reuse safety without any barrier: LL flags carry the call's sequence
+// number, and every slot set is double-buffered by seq parity
+// (nvrar.hpp:107-109,124-126). A rank can only write parity p again in call
+// k+2 after finishing call k+1, which needed data the reader sent only after
+// it had finished call k — so a slot is never overwritten before it is read.
+#include <cuda_runtime.h>
+
+#include "nvrar_device.cuh"
+
+namespace nvrar {
+
+__device__ __forceinline__ void publish_seq_len(const RankDesc& d, int peer, uint32_t seq,
+                                                uint64_t n) {
+  st_volatile64(counters(d, peer) + d.rank,
+                (static_cast<uint64_t>(seq) << 32) | (n & 0xFFFFFFFFull));
+}
+
+// wait_counter_ge(counters[peer], seq<<32) + check_peer_length
+// (transport.hpp:227-237, ring.hpp:90-98).
+__device__ __forceinline__ void wait_seq_len(Ctl& c, const RankDesc& d, int peer, uint64_t n) {
+  const uint64_t* p = counters(d, d.rank) + peer;
+  while (true) {
+    const uint64_t v = ld_volatile64(p);
+    const uint32_t s = static_cast<uint32_t>(v >> 32);
+    if (s == c.seq) {
+      if ((v & 0xFFFFFFFFull) != (n & 0xFFFFFFFFull)) {
+        record_fault(c, kProtocolFault, kLenMismatch, peer, 0, v);
+      }
+      return;
+    }
+    if (flag_ahead(s, c.seq)) return;
+    if (wait_tick(c, kSeqWait, peer, 0, v)) return;
+  }
+}
+
+__device__ __forceinline__ void finish_call(const RankDesc& d, uint32_t seq) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    RankState* st = d.state;
+    if (atomicAdd(&st->done, 1u) == gridDim.x - 1) {
+      st->done = 0;
+      st->seq = seq;
+      __threadfence();
+    }
+  }
+}
+
+template <int N>
+struct Log2 {
+  static constexpr int value = N <= 1 ? 0 : 1 + Log2<N / 2>::value;
+};
+template <>
+struct Log2<1> {
+  static constexpr int value = 0;
+};
+
+constexpr int kHierMaxG = 8;
+constexpr int kHierUpt = 2;  // units per thread carried through the RD steps together
+
+// ---------------------------------------------------------------------------
+template <class E, int N>
+__global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant__ LaunchParams lp) {
+  using A = typename E::acc;
+  constexpr int DW = E::DW;
+  constexpr int kSteps = Log2<N>::value;
+  const RankDesc& d = *lp.desc[blockIdx.y];
+  Ctl c;
+  c.d = &d;
+  c.spins = 0;
+  c.aborted = false;
+  if (ld_volatile32(&d.state->err.code) != 0u) return;  // sticky fault: comm is dead
+  c.t0 = globaltimer();
+  c.seq = ld_volatile32(&d.state->seq) + 1u;
+  const uint32_t parity = c.seq & 1u;
+
+  const uint64_t n = lp.count;
+  const int G = d.gpus, me = d.rank, node = d.node, local = d.local;
+  const uint64_t S = (n + G - 1) / G;
+  const uint64_t U = (S + kUnit - 1) / kUnit;
+  const uint64_t ub = U * blockIdx.x / gridDim.x;
+  const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
+  const void* send = lp.send[blockIdx.y];
+  void* recv = lp.recv[blockIdx.y];
+
+  // Peer-only sync, publish half (nvrar.hpp:163-171).
+  if (kSteps > 0 && blockIdx.x == 0 && threadIdx.x < kSteps) {
+    publish_seq_len(d, ((node ^ (1 << threadIdx.x)) * G) + local, c.seq, n);
+  }
+
+  // Phase 1a: reduce-scatter pushes (ring_reduce_scatter_phase, ring_schedule.hpp:33-58).
+  if (G > 1) {
+    for (int j = 1; j < G; ++j) {
+      const int cc = (local + j) % G;
+      uint4* slot = slot_a(d, node * G + cc, parity, local);
+      const uint64_t cbase = static_cast<uint64_t>(cc) * S;
+      for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+        const uint64_t e = cbase + kUnit * u;
+        const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e));
+        if (valid == 0) continue;  // pure padding: skipped identically by the reader
+        uint32_t raw[DW];
+        load_raw<E>(send, e, valid, raw);
+        ll_store<DW>(slot, u, raw, c.seq);
+      }
+    }
+  }
+
+  // Peer-only sync, wait half: all log2(N) XOR peers before any RD send.
+  if (kSteps > 0) {
+    if (threadIdx.x < kSteps) {
+      wait_seq_len(c, d, ((node ^ (1 << threadIdx.x)) * G) + local, n);
+    }
+    __syncthreads();
+  }
+
+  // Phases 1b+2+3a: fold own chunk, recursive doubling, cast + all-gather push.
+  const uint64_t mybase = static_cast<uint64_t>(local) * S;
+  for (uint64_t u0 = ub + threadIdx.x; u0 < ue; u0 += static_cast<uint64_t>(blockDim.x) * kHierUpt) {
+    A f[kHierUpt][4];
+    int valid[kHierUpt];
+    uint64_t uu[kHierUpt];
+#pragma unroll
+    for (int k = 0; k < kHierUpt; ++k) {
+      uu[k] = u0 + static_cast<uint64_t>(k) * blockDim.x;
+      valid[k] = uu[k] < ue ? clamp_valid(static_cast<int64_t>(n) -
+                                          static_cast<int64_t>(mybase + kUnit * uu[k]))
+                            : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kHierUpt; ++k) {
+      if (valid[k] == 0) continue;
+      uint32_t own[DW];
+      load_raw<E>(send, mybase + kUnit * uu[k], valid[k], own);
+      if (G == 1) {
+        raw_to_acc(E{}, own, f[k]);
+        continue;
+      }
+      uint32_t r[kHierMaxG - 1][DW];
+      bool ok[kHierMaxG - 1];
+      uint32_t bad = 0;
+#pragma unroll
+      for (int j = 1; j < kHierMaxG; ++j) {
+        if (j < G) ok[j - 1] = ll_try<DW>(slot_a(d, me, parity, (local + j) % G), uu[k], c.seq,
+                                          r[j - 1], bad);
+      }
+#pragma unroll
+      for (int j = 1; j < kHierMaxG; ++j) {
+        if (j < G && !ok[j - 1]) {
+          const int s = (local + j) % G;
+          ll_wait<DW>(c, slot_a(d, me, parity, s), uu[k], r[j - 1], node * G + s);
+        }
+      }
+      // c owns in[c] + (in[c-1] + (... + (in[c+2] + in[c+1])))  (ring_schedule.hpp:12-15)
+      raw_to_acc(E{}, r[0], f[k]);
+#pragma unroll
+      for (int j = 2; j < kHierMaxG; ++j) {
+        if (j < G) {
+          A a[4];
+          raw_to_acc(E{}, r[j - 1], a);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) f[k][q] = acc_add(f[k][q], a[q]);
+        }
+      }
+      A a[4];
+      raw_to_acc(E{}, own, a);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[k][q] = acc_add(f[k][q], a[q]);
+    }
+
+    // Recursive doubling (rd_block, nvrar.hpp:197-220): v = partner + own.
+#pragma unroll
+    for (int l = 0; l < kSteps; ++l) {
+      const int partner = ((node ^ (1 << l)) * G) + local;
+      uint4* dst = slot_c(d, partner, parity, l);
+#pragma unroll
+      for (int k = 0; k < kHierUpt; ++k) {
+        if (valid[k] == 0) continue;
+        uint32_t b[4];
+        acc_bits(f[k], b);
+        ll_store<4>(dst, uu[k], b, c.seq);
+      }
+      const uint4* src = slot_c(d, me, parity, l);
+#pragma unroll
+      for (int k = 0; k < kHierUpt; ++k) {
+        if (valid[k] == 0) continue;
+        uint32_t b[4];
+        ll_wait<4>(c, src, uu[k], b, partner);
+        A p[4];
+        bits_acc(b, p);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) f[k][q] = acc_add(p[q], f[k][q]);
+      }
+    }
+
+    // Final cast, own output, all-gather push (ring_all_gather_phase, ring_schedule.hpp:62-83).
+#pragma unroll
+    for (int k = 0; k < kHierUpt; ++k) {
+      if (valid[k] == 0) continue;
+      uint32_t o[DW];
+      acc_to_raw(E{}, f[k], o);
+      store_raw<E>(recv, mybase + kUnit * uu[k], valid[k], o);
+      for (int j = 1; j < G; ++j) {
+        ll_store<DW>(slot_b(d, node * G + (local + j) % G, parity, local), uu[k], o, c.seq);
+      }
+    }
+  }
+
+  // Phase 3b: all-gather receive.
+  if (G > 1) {
+    for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+      uint32_t r[kHierMaxG - 1][DW];
+      bool ok[kHierMaxG - 1];
+      int valid[kHierMaxG - 1];
+      uint32_t bad = 0;
+#pragma unroll
+      for (int j = 1; j < kHierMaxG; ++j) {
+        if (j < G) {
+          const int s = (local + j) % G;
+          valid[j - 1] = clamp_valid(static_cast<int64_t>(n) -
+                                     static_cast<int64_t>(static_cast<uint64_t>(s) * S + kUnit * u));
+          ok[j - 1] = valid[j - 1] == 0 ||
+                      ll_try<DW>(slot_b(d, me, parity, s), u, c.seq, r[j - 1], bad);
+        }
+      }
+#pragma unroll
+      for (int j = 1; j < kHierMaxG; ++j) {
+        if (j < G) {
+          const int s = (local + j) % G;
+          if (!ok[j - 1]) ll_wait<DW>(c, slot_b(d, me, parity, s), u, r[j - 1], node * G + s);
+          if (valid[j - 1] > 0) {
+            store_raw<E>(recv, static_cast<uint64_t>(s) * S + kUnit * u, valid[j - 1], r[j - 1]);
+          }
+        }
+      }
+    }
+  }
+
+  finish_call(d, c.seq);
+}
+
+// ---------------------------------------------------------------------------
+// Flat schedules. MAXG bounds gpus_per_node so the N x MAXG source units live
+// in statically indexed registers.
+
+template <class E, int N, int MAXG>
+__device__ __forceinline__ typename E::acc pick(const uint32_t (&r)[N][MAXG][E::DW], int nn,
+                                                int idx, int k) {
+  using A = typename E::acc;
+  A v{};
+#pragma unroll
+  for (int t = 0; t < MAXG; ++t) {
+    if (t == idx) {
+      A a[4];
+      raw_to_acc(E{}, r[nn][t], a);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q == k) v = a[q];
+    }
+  }
+  return v;
+}
+
+template <class E, int N, int MAXG>
+__global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant__ LaunchParams lp) {
+  using A = typename E::acc;
+  constexpr int DW = E::DW;
+  const RankDesc& d = *lp.desc[blockIdx.y];
+  Ctl c;
+  c.d = &d;
+  c.spins = 0;
+  c.aborted = false;
+  if (ld_volatile32(&d.state->err.code) != 0u) return;
+  c.t0 = globaltimer();
+  c.seq = ld_volatile32(&d.state->seq) + 1u;
+  const uint32_t parity = c.seq & 1u;
+
+  const uint64_t n = lp.count;
+  const int G = d.gpus, P = d.world, me = d.rank;
+  const bool oneshot = lp.oneshot != 0;
+  const uint64_t SG = (n + G - 1) / G;
+  const uint64_t SP = oneshot ? ((n + 3) & ~3ull) : ((((n + P - 1) / P) + 3) & ~3ull);
+  const uint64_t U = SP / kUnit;
+  const uint64_t ub = U * blockIdx.x / gridDim.x;
+  const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
+  const void* send = lp.send[blockIdx.y];
+  void* recv = lp.recv[blockIdx.y];
+
+  if (blockIdx.x == 0) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      if (p != me) publish_seq_len(d, p, c.seq, n);
+    }
+  }
+
+  // Reduce-scatter pushes: the owner q of each sub-shard receives our copy.
+  for (int j = 1; j < P; ++j) {
+    const int q = (me + j) % P;
+    const uint64_t qbase = oneshot ? 0 : static_cast<uint64_t>(q) * SP;
+    uint4* slot = slot_a(d, q, parity, me);
+    for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+      const uint64_t e = qbase + kUnit * u;
+      const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e));
+      if (valid == 0) continue;
+      uint32_t raw[DW];
+      load_raw<E>(send, e, valid, raw);
+      ll_store<DW>(slot, u, raw, c.seq);
+    }
+  }
+
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    if (p != me) wait_seq_len(c, d, p, n);
+  }
+  __syncthreads();
+
+  const uint64_t mybase = oneshot ? 0 : static_cast<uint64_t>(me) * SP;
+  for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+    const uint64_t e0 = mybase + kUnit * u;
+    const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+    if (valid == 0) continue;
+    const int c0 = static_cast<int>(e0 / SG);
+    const int c3 = static_cast<int>((e0 + valid - 1) / SG);
+
+    // Every source's unit, in fold order relative to c0: r[nn][j] is the copy
+    // of local rank (c0+1+j) % G of node nn.
+    uint32_t r[N][MAXG][DW];
+    bool ok[N][MAXG];
+    uint32_t bad = 0;
+#pragma unroll
+    for (int nn = 0; nn < N; ++nn) {
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        ok[nn][j] = true;
+        if (j < G) {
+          const int s = nn * G + (c0 + 1 + j) % G;
+          if (s == me) {
+            load_raw<E>(send, e0, valid, r[nn][j]);
+          } else {
+            ok[nn][j] = ll_try<DW>(slot_a(d, me, parity, s), u, c.seq, r[nn][j], bad);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int nn = 0; nn < N; ++nn) {
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        if (j < G && !ok[nn][j]) {
+          const int s = nn * G + (c0 + 1 + j) % G;
+          ll_wait<DW>(c, slot_a(d, me, parity, s), u, r[nn][j], s);
+        }
+      }
+    }
+
+    A part[N][4];
+    if (c0 == c3) {
+#pragma unroll
+      for (int nn = 0; nn < N; ++nn) {
+        raw_to_acc(E{}, r[nn][0], part[nn]);
+#pragma unroll
+        for (int j = 1; j < MAXG; ++j) {
+          if (j < G) {
+            A a[4];
+            raw_to_acc(E{}, r[nn][j], a);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) part[nn][q] = acc_add(part[nn][q], a[q]);
+          }
+        }
+      }
+    } else {
+      // The unit straddles a shard boundary: per-element fold order.
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int cq = q < valid ? static_cast<int>((e0 + q) / SG) : c0;
+        const int rot = cq - c0;
+#pragma unroll
+        for (int nn = 0; nn < N; ++nn) {
+          A v = pick<E, N, MAXG>(r, nn, rot % G, q);
+#pragma unroll
+          for (int j = 1; j < MAXG; ++j) {
+            if (j < G) v = acc_add(v, pick<E, N, MAXG>(r, nn, (j + rot) % G, q));
+          }
+          part[nn][q] = v;
+        }
+      }
+    }
+    // Pairwise tree over nodes in node order == the XOR-step adds.
+#pragma unroll
+    for (int w = 1; w < N; w <<= 1) {
+#pragma unroll
+      for (int nn = 0; nn + w < N; nn += 2 * w) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) part[nn][q] = acc_add(part[nn][q], part[nn + w][q]);
+      }
+    }
+    uint32_t o[DW];
+    acc_to_raw(E{}, part[0], o);
+    store_raw<E>(recv, e0, valid, o);
+    if (!oneshot) {
+      for (int j = 1; j < P; ++j) ll_store<DW>(slot_b(d, (me + j) % P, parity, me), u, o, c.seq);
+    }
+  }
+
+  if (!oneshot) {
+    for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+      for (int j = 1; j < P; ++j) {
+        const int q = (me + P - j) % P;
+        const uint64_t e0 = static_cast<uint64_t>(q) * SP + kUnit * u;
+        const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+        if (valid == 0) continue;
+        uint32_t r[DW];
+        ll_wait<DW>(c, slot_b(d, me, parity, q), u, r, q);
+        store_raw<E>(recv, e0, valid, r);
+      }
+    }
+  }
+
+  finish_call(d, c.seq);
+}
+
+__global__ void seq_bump_kernel(const __grid_constant__ LaunchParams lp) {
+  const RankDesc& d = *lp.desc[blockIdx.y];
+  if (threadIdx.x == 0 && ld_volatile32(&d.state->err.code) == 0u) d.state->seq += 1u;
+}
+
+// ---------------------------------------------------------------------------
+// Dispatch
+
+using KernelFn = void (*)(LaunchParams);
+
+template <class E>
+KernelFn hier_for(int nodes) {
+  switch (nodes) {
+    case 1: return hier_kernel<E, 1>;
+    case 2: return hier_kernel<E, 2>;
+    case 4: return hier_kernel<E, 4>;
+    case 8: return hier_kernel<E, 8>;
+    default: return nullptr;
+  }
+}
+
+template <class E>
+KernelFn flat_for(int nodes) {
+  switch (nodes) {
+    case 1: return flat_kernel<E, 1, 8>;
+    case 2: return flat_kernel<E, 2, 8>;
+    case 4: return flat_kernel<E, 4, 4>;
+    case 8: return flat_kernel<E, 8, 2>;
+    default: return nullptr;
+  }
+}
+
+int flat_max_gpus(int nodes) {
+  switch (nodes) {
+    case 1: return 8;
+    case 2: return 8;
+    case 4: return 4;
+    case 8: return 2;
+    default: return 0;
+  }
+}
+
+KernelFn select_kernel(int dtype, bool flat, int nodes) {
+  switch (dtype) {
+    case 0: return flat ? flat_for<I32>(nodes) : hier_for<I32>(nodes);
+    case 1: return flat ? flat_for<F32>(nodes) : hier_for<F32>(nodes);
+    case 2: return flat ? flat_for<BF16>(nodes) : hier_for<BF16>(nodes);
+    default: return nullptr;
+  }
+}
+
+KernelFn bump_kernel() { return seq_bump_kernel; }
+
+}  // namespace nvrar
