@@ -88,6 +88,14 @@ struct Log2<1> {
   static constexpr int value = 0;
 };
 
+// Real elements of unit u of the chunk starting at cbase with S elements: the
+// chunk boundary (not only n) bounds it, since S need not be a multiple of 4.
+__device__ __forceinline__ int chunk_valid(uint64_t S, uint64_t u, uint64_t n, uint64_t cbase) {
+  const int64_t in_chunk = static_cast<int64_t>(S) - static_cast<int64_t>(kUnit * u);
+  const int64_t in_vec = static_cast<int64_t>(n) - static_cast<int64_t>(cbase + kUnit * u);
+  return clamp_valid(in_chunk < in_vec ? in_chunk : in_vec);
+}
+
 constexpr int kHierMaxG = 8;
 constexpr int kHierUpt = 2;  // units per thread carried through the RD steps together
 
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       const uint64_t cbase = static_cast<uint64_t>(cc) * S;
       for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
         const uint64_t e = cbase + kUnit * u;
-        const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e));
+        const int valid = chunk_valid(S, u, n, cbase);
         if (valid == 0) continue;  // pure padding: skipped identically by the reader
         uint32_t raw[DW];
         load_raw<E>(send, e, valid, raw);
@@ -155,9 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
       uu[k] = u0 + static_cast<uint64_t>(k) * blockDim.x;
-      valid[k] = uu[k] < ue ? clamp_valid(static_cast<int64_t>(n) -
-                                          static_cast<int64_t>(mybase + kUnit * uu[k]))
-                            : 0;
+      valid[k] = uu[k] < ue ? chunk_valid(S, uu[k], n, mybase) : 0;
     }
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
@@ -249,8 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G) {
           const int s = (local + j) % G;
-          valid[j - 1] = clamp_valid(static_cast<int64_t>(n) -
-                                     static_cast<int64_t>(static_cast<uint64_t>(s) * S + kUnit * u));
+          valid[j - 1] = chunk_valid(S, u, n, static_cast<uint64_t>(s) * S);
           ok[j - 1] = valid[j - 1] == 0 ||
                       ll_try<DW>(slot_b(d, me, parity, s), u, c.seq, r[j - 1], bad);
         }

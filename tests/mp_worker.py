@@ -1,0 +1,134 @@
+"""Multi-process, multi-GPU parity worker (one rank per GPU), launched by
+tests/test_multigpu.py through torch.distributed.run. Every rank regenerates
+all ranks' inputs with the oracle's generator, runs the CUDA all-reduce over
+NVLink (IPC-mapped peer regions), and checks its output against the oracle.
+
+    python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
+        tests/mp_worker.py --nodes 2 --gpus 2
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle as O  # noqa: E402
+from paper_2511_09557_b200 import ClusterTopology, Communicator, NvrarConfig  # noqa: E402
+from paper_2511_09557_b200 import _lib as L  # noqa: E402
+from paper_2511_09557_b200 import dist as D  # noqa: E402
+
+
+def to_dev(a, dtype):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype == "bf16":
+        t = t.view(torch.int16).view(torch.bfloat16)
+    return t.cuda()
+
+
+def from_dev(t, dtype):
+    if dtype == "bf16":
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def inputs(dtype, p, n, seed):
+    if dtype == "i32":
+        return O.random_inputs(p, n, seed, "i32")
+    x = O.random_inputs(p, n, seed, "f32")
+    return O.bf16_bits_from_f32(x) if dtype == "bf16" else x
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nodes", type=int, required=True)
+    ap.add_argument("--gpus", type=int, required=True)
+    ap.add_argument("--mismatch", action="store_true", help="length-mismatch protocol fault")
+    args = ap.parse_args()
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    topo = ClusterTopology(args.nodes, args.gpus)
+    assert topo.world_size() == world
+    comm = Communicator.from_process_group(topo, 4 << 20, device=local, timeout_s=20.0)
+    fails = 0
+    if args.mismatch:
+        comm.set_algo("hier" if args.nodes > 1 else "twoshot")
+        n = 1024 + (1 if rank == 0 else 0)
+        x = torch.ones(n, device="cuda")
+        comm.allreduce(x, x)
+        rc = comm.check_status()
+        ok = rc in (L.ERR_PROTOCOL_FAULT, L.ERR_DEADLOCK)
+        print(f"rank {rank}: mismatch status {rc} ({comm.last_error()})", flush=True)
+        dist.barrier()
+        sys.exit(0 if ok else 1)
+
+    algos = ["hier", "twoshot", "oneshot"]
+    for dtype in ("f32", "bf16", "i32"):
+        for algo in algos:
+            comm.set_algo(algo)
+            for n in (1, 1031, 65539, 262144):
+                x = inputs(dtype, world, n, 1000 + n)
+                want = O.nvrar_order_sum(x, args.nodes, args.gpus,
+                                         {"f32": "f32", "bf16": "bf16", "i32": "i32"}[dtype])
+                inp = to_dev(x[rank], dtype)
+                out = torch.empty_like(inp)
+                plan = D.plan_consensus(comm.plan(n, inp.dtype))
+                comm.allreduce(inp, out)
+                torch.cuda.synchronize()
+                comm.check()
+                got = from_dev(out, dtype)
+                if dtype == "f32":
+                    got, want = got.view(np.uint32), want.view(np.uint32)
+                bad = int(np.count_nonzero(got != want))
+                if bad:
+                    fails += 1
+                    print(f"rank {rank}: {dtype} {algo} {plan} n={n}: {bad} mismatches", flush=True)
+    # back-to-back calls captured in a CUDA graph, replayed (seq lives on the device)
+    comm.set_algo("auto")
+    comm.set_config(NvrarConfig())
+    n = 1 << 19
+    xs = [inputs("bf16", world, n, 7000 + c) for c in range(4)]
+    ins = [to_dev(x[rank], "bf16") for x in xs]
+    outs = [torch.empty_like(t) for t in ins]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for c in range(4):  # warm-up outside capture
+            comm.allreduce(ins[c], outs[c], stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    seq0 = comm.sequence()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for c in range(4):
+            comm.allreduce(ins[c], outs[c])
+    for _ in range(25):
+        for o in outs:
+            o.zero_()
+        graph.replay()
+    torch.cuda.synchronize()
+    comm.check()
+    seq1 = comm.sequence()
+    if seq1 - seq0 != 100:
+        fails += 1
+        print(f"rank {rank}: sequence advanced by {seq1 - seq0}, expected 100", flush=True)
+    for c in range(4):
+        want = O.nvrar_order_sum(xs[c], args.nodes, args.gpus, "bf16")
+        if not np.array_equal(from_dev(outs[c], "bf16"), want):
+            fails += 1
+            print(f"rank {rank}: graph replay call {c} differs", flush=True)
+    print(f"rank {rank}: {'OK' if fails == 0 else f'{fails} FAILURES'}", flush=True)
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,55 @@
+"""Real multi-process, multi-GPU runs (one rank per B200, IPC-mapped peers over
+NVLink/NVSwitch). Skipped unless at least 2 devices are visible."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NDEV = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+TOPOS = {2: [(2, 1), (1, 2)], 4: [(2, 2), (4, 1), (1, 4)],
+         8: [(2, 4), (4, 2), (8, 1), (1, 8)]}
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(world, nodes, gpus, extra=()):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tests", "mp_worker.py"),
+           "--nodes", str(nodes), "--gpus", str(gpus), *extra]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    return r.returncode, r.stdout + r.stderr
+
+
+CASES = [(w, n, g) for w in (2, 4, 8) for (n, g) in TOPOS[w]]
+
+
+@pytest.mark.parametrize("world,nodes,gpus", CASES)
+def test_multiprocess_parity(world, nodes, gpus):
+    if NDEV < world:
+        pytest.skip(f"needs {world} GPUs, have {NDEV}")
+    rc, out = _run(world, nodes, gpus)
+    assert rc == 0, out[-4000:]
+    assert out.count(": OK") == world, out[-4000:]
+
+
+@pytest.mark.parametrize("nodes,gpus", [(2, 1), (1, 2)])
+def test_length_mismatch_is_protocol_fault(nodes, gpus):
+    if NDEV < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, nodes, gpus, ("--mismatch",))
+    assert rc == 0, out[-4000:]
+    assert "status 4" in out, out[-4000:]
