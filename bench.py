@@ -1,0 +1,472 @@
+"""NVRAR all-reduce benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nvrar|reference]
+
+N=1  : BASELINE configs[0] on one B200 — 8 ranks as 2 virtual nodes x 4, 1 MB
+       fp32 sum; the 8 ranks are virtual ranks on cuda:0 (one cooperative
+       launch, all ranks' buffers in one HBM), the GPU analogue of the
+       reference running all ranks in one process.
+N>1  : launched by torch.distributed.run, one rank per GPU; hierarchy 2 x N/2
+       (N=8: 2x4, configs[1]); headline message 1 MB bf16, plus the 64 KB-8 MB
+       sweep against NCCL all-reduce on the same buffers (configs[1]/[2]).
+
+A "step" is one CUDA-graph replay of `calls` back-to-back all-reduces over
+rotating buffers whose total exceeds the 126 MB L2 (so no call reads an input
+left in L2 by an earlier one). Per-step time comes from CUDA events on the
+launching stream, the max over ranks is taken per step, and the per-call
+latency is step / calls; `value` is the p50 over the K timed steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 << 20
+ROTATE_BYTES = 160 << 20   # > L2: rotating input+output footprint per GPU
+METRIC = "all-reduce p50 latency (µs, max over ranks) 128KB–2MB at 2/4/8 B200 vs NCCL"
+NVLINK_PEAK_GBS = 770.0    # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+NVLINK_NOMINAL_GBS = 900.0
+SWEEP = [64 << 10, 128 << 10, 256 << 10, 512 << 10, 1 << 20, 2 << 20, 4 << 20, 8 << 20]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---- clocks sampled during the timed region --------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---- graph timing -------------------------------------------------------------------
+
+def graph_of(torch, fn, calls, stream):
+    """Capture `calls` back-to-back invocations fn(i) into one CUDA graph."""
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        for i in range(min(calls, 4)):
+            fn(i)
+    torch.cuda.current_stream().wait_stream(stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(calls):
+            fn(i)
+    torch.cuda.synchronize()
+    return g
+
+
+def time_steps(torch, replay, steps, warmup, barrier, stream):
+    """Per-step device time (ms) of `replay()` with events on `stream`."""
+    for _ in range(warmup):
+        with torch.cuda.stream(stream):
+            replay()
+    torch.cuda.synchronize()
+    times = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for a, b in ev:
+            a.record(stream)
+            replay()
+            b.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    for a, b in ev:
+        times.append(a.elapsed_time(b))
+    return times
+
+
+# ---- the CPU reference path ---------------------------------------------------------
+
+def cpu_reference(nodes, gpus, n, budget_s=12.0, max_calls=60):
+    """ccsim::NvrarAllreduce<float> on the reference's ConcurrentEngine (oracle/_ref,
+    compiled from the reference sources), pre-generated inputs, per-call makespan."""
+    from oracle import oracle as O
+    x = O.random_inputs(nodes * gpus, n, 1234, "f32")
+    kind = "reference" if O.ref_available() else "port"
+    if kind == "port":
+        # the C restatement (single thread) of the same arithmetic
+        t0 = time.perf_counter()
+        calls = 0
+        per = []
+        while calls < max_calls and time.perf_counter() - t0 < budget_s:
+            t = time.perf_counter()
+            O.nvrar_order_sum(x, nodes, gpus)
+            per.append((time.perf_counter() - t) * 1e6)
+            calls += 1
+        return statistics.median(per), kind, 1, f"{calls} calls, {nodes}x{gpus}, n={n} fp32"
+    t0 = time.perf_counter()
+    per = list(O.ref_time_concurrent(x, nodes, gpus, warmup=2, calls=3))
+    one = (time.perf_counter() - t0) / 5
+    more = int(max(0, min(max_calls, budget_s / max(one, 1e-6)) - 5))
+    if more > 0:
+        per += list(O.ref_time_concurrent(x, nodes, gpus, warmup=1, calls=more))
+    threads = nodes * gpus  # one std::thread per rank (concurrent_transport.hpp:59-75)
+    return (statistics.median(per), kind, min(threads, os.cpu_count() or threads),
+            f"{len(per)} calls of NvrarAllreduce<float> on ConcurrentEngine, {nodes}x{gpus}, "
+            f"n={n} fp32, B=1, C=65536, p50 of per-call makespan (host nproc={os.cpu_count()})")
+
+
+# ---- arms ---------------------------------------------------------------------------------
+
+def hier_for(world):
+    return {1: (2, 4), 2: (2, 1), 4: (2, 2), 8: (2, 4)}[world]
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    nodes, gpus = hier_for(world)
+    n = (1 << 20) // 4 if world == 1 else (1 << 20) // 2
+    per = []
+    t0 = time.perf_counter()
+    for _ in range(args.warmup):
+        cpu_reference(nodes, gpus, n, budget_s=2.0, max_calls=3)
+    for _ in range(args.steps):
+        v, kind, cores, sample = cpu_reference(nodes, gpus, n, budget_s=4.0, max_calls=10)
+        per.append(v)
+    total = time.perf_counter() - t0
+    val = statistics.median(per)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "us",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total * 1e3 / max(1, args.steps + args.warmup), 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (oracles::random_inputs, seed 1234)",
+        "config": {"workload": f"reference CPU NVRAR all-reduce, {nodes}x{gpus} ranks as threads, "
+                               f"{n} fp32 elements (the element count of the GPU arm's message)",
+                   "nodes": nodes, "gpus_per_node": gpus, "elements": n},
+        "cpu_baseline": {"value": round(val, 3), "unit": "us", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(val, 3), "unit": "us", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def calls_for(msg_bytes, ranks_on_gpu):
+    per_call = 2 * msg_bytes * ranks_on_gpu
+    return int(min(1000, max(50, math.ceil(ROTATE_BYTES / per_call))))
+
+
+def run_emulated(args):
+    """N=1: configs[0] with 8 virtual ranks on cuda:0."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+    from paper_2511_09557_b200 import ClusterTopology, LocalGroup, NvrarConfig
+    from paper_2511_09557_b200 import _lib as L
+
+    nodes, gpus = 2, 4
+    P = nodes * gpus
+    msg = 1 << 20
+    n = msg // 4
+    calls = calls_for(msg, P)
+    g = LocalGroup(ClusterTopology(nodes, gpus), max(msg, 8 << 20), device=0, timeout_s=30.0)
+    algo, blocks = g.comms[0].plan(n, torch.float32)
+    x = O.random_inputs(P, n, 1234, "f32")
+    base_in = [torch.from_numpy(x[r]).cuda() for r in range(P)]
+    sets = []
+    for _ in range(calls):
+        ins = [t.clone() for t in base_in]
+        outs = [torch.empty_like(t) for t in base_in]
+        sets.append((ins, outs))
+    stream = torch.cuda.Stream()
+
+    def call(i):
+        ins, outs = sets[i]
+        g.launch(ins, outs, stream=torch.cuda.current_stream())
+
+    graph = graph_of(torch, call, calls, stream)
+    hbm, hbm_kind = peaks()
+    with ClockSampler(0) as clk:
+        times = time_steps(torch, graph.replay, args.steps, args.warmup, lambda: None, stream)
+    g.check()
+    want = O.nvrar_order_sum(x, nodes, gpus).view(np.uint32)
+    for r in range(P):
+        assert np.array_equal(sets[-1][1][r].cpu().numpy().view(np.uint32), want), "parity"
+    per_call_us = [t * 1e3 / calls for t in times]
+    p50 = statistics.median(per_call_us)
+    # roofline: every rank's input read + output written once from HBM (2*P*M)
+    alg_bytes = 2 * P * msg
+    achieved = alg_bytes / (p50 * 1e-6) / 1e9
+
+    # e2e through the public API with host buffers (pinned): H2D of the 8 inputs,
+    # the all-reduce, D2H of the 8 outputs, every step.
+    host_in = [torch.from_numpy(x[r]).pin_memory() for r in range(P)]
+    host_out = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(P)]
+    dev_in, dev_out = sets[0]
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            for r in range(P):
+                dev_in[r].copy_(host_in[r], non_blocking=True)
+            g.launch(dev_in, dev_out, stream=stream)
+            for r in range(P):
+                host_out[r].copy_(dev_out[r], non_blocking=True)
+            b.record(stream)
+        b.synchronize()
+        if k >= args.warmup:
+            e2e.append(a.elapsed_time(b) * 1e3)
+    g.check()
+    assert np.array_equal(host_out[0].numpy().view(np.uint32), want)
+
+    # bf16 sweep on the same virtual group (context for the configs[1] sizes)
+    sweep = {}
+    if not args.no_sweep:
+        for size in (128 << 10, 512 << 10, 2 << 20):
+            ne = size // 2
+            c2 = calls_for(size, P)
+            xs = [torch.randn(ne, device="cuda").to(torch.bfloat16) for _ in range(P)]
+            st = [([t.clone() for t in xs], [torch.empty_like(t) for t in xs]) for _ in range(c2)]
+            gr = graph_of(torch, lambda i: g.launch(*st[i], stream=torch.cuda.current_stream()),
+                          c2, stream)
+            ts = time_steps(torch, gr.replay, max(5, args.steps // 2), 2, lambda: None, stream)
+            sweep[f"{size >> 10}KB_bf16"] = {"p50_us": round(statistics.median(ts) * 1e3 / c2, 3),
+                                             "algo": g.comms[0].plan(ne, torch.bfloat16)[0]}
+            del gr, st
+    g.check()
+
+    cpu_v, cpu_kind, cpu_cores, cpu_sample = cpu_reference(nodes, gpus, n)
+    line = {
+        "metric": METRIC, "value": round(p50, 3), "unit": "us", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(statistics.mean(times), 4), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (oracles::random_inputs, seed 1234); output checked bit-exact vs oracle",
+        "config": {"workload": "configs[0]: 2x4 virtual nodes (8 ranks as virtual ranks on one "
+                               "B200, one cooperative launch per all-reduce), 1 MB fp32 sum",
+                   "nodes": nodes, "gpus_per_node": gpus, "message_bytes": msg, "algo": algo,
+                   "blocks_per_rank": blocks, "calls_per_step": calls,
+                   "l2": f"rotating buffers, {calls} x 16 MB per step > 126 MB L2",
+                   "p10_us": round(sorted(per_call_us)[len(per_call_us) // 10], 3),
+                   "p90_us": round(sorted(per_call_us)[(9 * len(per_call_us)) // 10], 3)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                     "peak_kind": hbm_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                     "traffic": None,
+                     "algorithmic_bytes": alg_bytes,
+                     "note": "emulated ranks share one HBM: 2*P*M bytes (all inputs read, all "
+                             "outputs written) per launch"},
+        "cpu_baseline": {"value": round(cpu_v, 3), "unit": "us", "cores": cpu_cores,
+                         "kind": cpu_kind, "sample": cpu_sample},
+        "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
+                "h2d_bytes_per_step": P * msg, "d2h_bytes_per_step": P * msg},
+        "gpu_launches": (args.steps + args.warmup) * calls,
+        "clocks": clk.summary(),
+        "sweep": sweep,
+    }
+    print(json.dumps(line), flush=True)
+    g.close()
+
+
+def run_multi(args, rank, world, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_09557_b200 import ClusterTopology, Communicator
+    from paper_2511_09557_b200 import dist as D
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nodes, gpus = hier_for(world)
+    comm = Communicator.from_process_group(ClusterTopology(nodes, gpus), 8 << 20, device=local,
+                                           timeout_s=30.0)
+    stream = torch.cuda.Stream()
+    barrier = lambda: dist.barrier(device_ids=[local])  # noqa: E731
+
+    def measure(msg, dtype, impl, steps, warmup, algo="auto"):
+        ne = msg // (2 if dtype == torch.bfloat16 else 4)
+        calls = calls_for(msg, 1)
+        torch.manual_seed(1234 + rank)
+        src = torch.randn(ne, device="cuda").to(dtype)
+        bufs = [(src.clone(), torch.empty_like(src)) for _ in range(calls)]
+        if impl == "nvrar":
+            comm.set_algo(algo)
+            plan = D.plan_consensus(comm.plan(ne, dtype))
+            fn = lambda i: comm.allreduce(bufs[i][0], bufs[i][1])  # noqa: E731
+        else:
+            plan = ("nccl", 0)
+            fn = lambda i: dist.all_reduce(bufs[i][1])  # noqa: E731
+            for a, b in bufs:
+                b.copy_(a)
+        gr = graph_of(torch, fn, calls, stream)
+        ts = time_steps(torch, gr.replay, steps, warmup, barrier, stream)
+        ts = D.max_over_ranks(ts, device=torch.device("cuda", local))
+        if impl == "nvrar":
+            comm.check()
+        del gr
+        per = [t * 1e3 / calls for t in ts]
+        return statistics.median(per), per, calls, plan
+
+    hbm, hbm_kind = peaks()
+    msg = 1 << 20
+    with ClockSampler(local) as clk:
+        p50, per, calls, plan = measure(msg, torch.bfloat16, "nvrar", args.steps, args.warmup)
+    nccl50, _, _, _ = measure(msg, torch.bfloat16, "nccl", args.steps, args.warmup)
+
+    # e2e: pinned host input -> device, all-reduce, device -> host, per step; max over ranks
+    ne = msg // 2
+    host_in = torch.randn(ne).to(torch.bfloat16).pin_memory()
+    host_out = torch.empty(ne, dtype=torch.bfloat16).pin_memory()
+    din = torch.empty(ne, dtype=torch.bfloat16, device="cuda")
+    dout = torch.empty_like(din)
+    comm.set_algo("auto")
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            din.copy_(host_in, non_blocking=True)
+            comm.allreduce(din, dout, stream=stream)
+            host_out.copy_(dout, non_blocking=True)
+            b.record(stream)
+        b.synchronize()
+        if k >= args.warmup:
+            e2e.append(a.elapsed_time(b) * 1e3)
+    e2e = D.max_over_ranks(e2e, device=torch.device("cuda", local))
+    comm.check()
+
+    sweep = {}
+    if not args.no_sweep:
+        for size in SWEEP:
+            s_steps = max(5, args.steps // 2)
+            v, _, _, pl = measure(size, torch.bfloat16, "nvrar", s_steps, 2)
+            nv, _, _, _ = measure(size, torch.bfloat16, "nccl", s_steps, 2)
+            row = {"nvrar_us": round(v, 3), "nccl_us": round(nv, 3), "algo": pl[0],
+                   "blocks": pl[1], "speedup_vs_nccl": round(nv / v, 3)}
+            for forced in ("hier", "twoshot", "oneshot"):
+                if forced == "oneshot" and size > (1 << 20):
+                    continue
+                fv, _, _, _ = measure(size, torch.bfloat16, "nvrar", s_steps, 2, algo=forced)
+                row[f"{forced}_us"] = round(fv, 3)
+            b_alg = 2 * (world - 1) / world * size
+            row["busbw_GBs"] = round(b_alg / (v * 1e-6) / 1e9, 1)
+            row["bw_floor_us"] = round(b_alg / (NVLINK_NOMINAL_GBS * 1e9) * 1e6, 3)
+            sweep[f"{size >> 10}KB"] = row
+            comm.set_algo("auto")
+
+    b_alg = 2 * (world - 1) / world * msg
+    busbw = b_alg / (p50 * 1e-6) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(p50, 3), "unit": "us", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(statistics.mean(per) * calls / 1e3, 4),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (torch.randn, seed 1234+rank)",
+            "config": {"workload": f"NVRAR bf16 sum, {world} B200 as {nodes}x{gpus} virtual "
+                                   f"nodes, 1 MB message (configs[1] sweep point)",
+                       "nodes": nodes, "gpus_per_node": gpus, "message_bytes": msg,
+                       "algo": plan[0], "blocks_per_rank": plan[1], "calls_per_step": calls,
+                       "l2": f"rotating buffers, {calls} x 2 MB per step > 126 MB L2",
+                       "nccl_p50_us": round(nccl50, 3),
+                       "speedup_vs_nccl": round(nccl50 / p50, 3)},
+            "roofline": {"bound": "nvlink", "achieved": round(busbw, 1),
+                         "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                         "frac": round(busbw / NVLINK_PEAK_GBS, 4), "traffic": None,
+                         "algorithmic_bytes": b_alg,
+                         "note": "busbw = 2(P-1)/P*M / t (nccl-tests convention); peak = measured "
+                                 "B200 peer copy per direction (900 nominal)"},
+            "cpu_baseline": None,
+            "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
+                    "h2d_bytes_per_step": msg, "d2h_bytes_per_step": msg},
+            "gpu_launches": (args.steps + args.warmup) * calls,
+            "clocks": clk.summary(),
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    barrier()
+    comm.close()
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["nvrar", "reference"], default="nvrar")
+    ap.add_argument("--no-sweep", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world == 1:
+        run_emulated(args)
+    else:
+        run_multi(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()
