@@ -333,6 +333,7 @@ def run_multi(args, rank, world, local):
     from paper_2511_09557_b200 import dist as D
 
     torch.cuda.set_device(local)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nodes, gpus = hier_for(world)
     comm = Communicator.from_process_group(ClusterTopology(nodes, gpus), 8 << 20, device=local,

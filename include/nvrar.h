@@ -165,6 +165,15 @@ int nvrar_get_peers(nvrar_comm_t comm, int* peers, int max_peers, int* steps);
 /* Synchronises the device and returns the sticky device status (0 = ok). */
 int nvrar_check(nvrar_comm_t comm);
 int nvrar_get_blocked(nvrar_comm_t comm, nvrar_blocked_t* out);
+/* Diagnostics: phase timestamps (globaltimer ns) of CTA 0 of the last call,
+ * recorded when profiling is on; and the NVLink signal latency probe — a flag
+ * ping-pong with `peer` (both ranks call it; one with initiator = 1), which
+ * returns the initiator's elapsed ns for `iters` round trips (alpha_signal =
+ * elapsed / iters / 2, the latency floor of the roofline). */
+int nvrar_set_profile(nvrar_comm_t comm, int on);
+int nvrar_get_phase_times(nvrar_comm_t comm, uint64_t* ts, int n);
+int nvrar_pingpong(nvrar_comm_t comm, int peer, int iters, int initiator, void* stream,
+                   uint64_t* elapsed_ns);
 const char* nvrar_last_error(nvrar_comm_t comm);
 const char* nvrar_status_string(int status);
 int nvrar_abi_version(void);

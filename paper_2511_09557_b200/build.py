@@ -14,8 +14,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libnvrar_b200.so")
-SOURCES = ["nvrar_kernels.cu", "nvrar_comm.cu"]
-HEADERS = ["nvrar_device.cuh", os.path.join("..", "..", "include", "nvrar.h")]
+SOURCES = ["nvrar_inst_f32.cu", "nvrar_inst_bf16.cu", "nvrar_inst_i32.cu", "nvrar_misc.cu",
+           "nvrar_comm.cu"]
+HEADERS = ["nvrar_device.cuh", "nvrar_kernels.cuh", os.path.join("..", "..", "include", "nvrar.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -38,8 +39,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -50,7 +52,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         with open(obj + ".ptxas.txt", "w") as fh:
             fh.write(r.stderr)
-        objs.append(obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     subprocess.check_call(cmd)

@@ -18,8 +18,10 @@
 
 namespace nvrar {
 using KernelFn = void (*)(LaunchParams);
-KernelFn select_kernel(int dtype, bool flat, int nodes);
+KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu);
 KernelFn bump_kernel();
+using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);
+PingFn pingpong_fn();
 int flat_max_gpus(int nodes);
 }  // namespace nvrar
 
@@ -77,6 +79,9 @@ struct nvrar_comm {
   int sticky = 0;
   std::string last_error;
   int max_ctas = 148;  // co-resident CTAs of one kernel on this device
+  bool pdl = true;     // programmatic dependent launch for single-rank launches
+  uint64_t pp_base = 0;
+  uint64_t* d_scratch = nullptr;
 };
 
 namespace {
@@ -270,6 +275,7 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
       (e = cudaMalloc(&c->state, sizeof(RankState))) != cudaSuccess ||
       (e = cudaMemset(c->state, 0, sizeof(RankState))) != cudaSuccess ||
       (e = cudaMalloc(&c->d_desc, sizeof(RankDesc))) != cudaSuccess ||
+      (e = cudaMalloc(&c->d_scratch, 64)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess) {
     fail(c, NVRAR_ERR_CUDA, "allocating %llu B symmetric region: %s",
          static_cast<unsigned long long>(c->lay.bytes), cudaGetErrorString(e));
@@ -279,16 +285,19 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   for (int flat = 0; flat < 2; ++flat) {
     for (int dt = 0; dt < 3; ++dt) {
-      int o = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-              &o, reinterpret_cast<const void*>(select_kernel(dt, flat, c->nodes)), kThreads,
-              0) == cudaSuccess &&
-          o > 0) {
-        occ = flat + dt == 0 ? o : std::min(occ, o);
+      for (int emu = 0; emu < 2; ++emu) {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &o, reinterpret_cast<const void*>(select_kernel(dt, flat, c->nodes, emu)),
+                kThreads, 0) == cudaSuccess &&
+            o > 0) {
+          occ = flat + dt + emu == 0 ? o : std::min(occ, o);
+        }
       }
     }
   }
-  c->max_ctas = std::max(1, sms * std::max(occ, 1));
+  c->max_ctas = std::max(1, std::min(kSeqSlots, sms * std::max(occ, 1)));
+  if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
   c->h_desc = RankDesc{};
   c->h_desc.state = c->state;
   c->h_desc.lay = c->lay;
@@ -414,6 +423,7 @@ int nvrar_finalize(nvrar_comm_t c) {
   if (c->region) cudaFree(c->region);
   if (c->state) cudaFree(c->state);
   if (c->d_desc) cudaFree(c->d_desc);
+  if (c->d_scratch) cudaFree(c->d_scratch);
   delete c;
   return NVRAR_SUCCESS;
 }
@@ -535,19 +545,34 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   }
   int algo = 0, blocks = 1;
   plan(c0, count, dtype, &algo, &blocks);
-  if (local_group) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  const bool emu = local_group;
+  if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
-  KernelFn k = select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes);
+  if (!emu) lp.d0 = c0->h_desc;  // by value: the kernel reads it from param space
+  KernelFn k = select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu);
   if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
-  dim3 grid(blocks, nl), block(kThreads);
-  if (local_group && nl > 1) {
-    void* args[] = {&lp};
-    CUDA_TRY(c0, cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), grid, block, args,
-                                             0, s));
-  } else {
-    k<<<grid, block, 0, s>>>(lp);
-    CUDA_TRY(c0, cudaGetLastError());
+
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks, nl);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 0;
+  if (emu) {
+    // virtual ranks wait on each other: all CTAs must be co-resident
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.numAttrs = 1;
+  } else if (c0->pdl) {
+    // overlap this launch with the tail of the previous kernel on the stream;
+    // the kernel's griddepcontrol.wait keeps every data access after it
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 1;
   }
+  CUDA_TRY(c0, cudaLaunchKernelEx(&cfg, k, lp));
   return NVRAR_SUCCESS;
 }
 
@@ -574,7 +599,46 @@ int nvrar_get_sequence(nvrar_comm_t c, uint32_t* seq) {
   CUDA_TRY(c, cudaDeviceSynchronize());
   RankState st;
   CUDA_TRY(c, cudaMemcpy(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
-  *seq = st.seq;
+  *seq = st.seq[0];
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_set_profile(nvrar_comm_t c, int on) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  c->h_desc.profile = on ? 1 : 0;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpy(c->d_desc, &c->h_desc, sizeof(RankDesc), cudaMemcpyHostToDevice));
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_get_phase_times(nvrar_comm_t c, uint64_t* ts, int n) {
+  if (!c || !ts || n < 1) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  RankState st;
+  CUDA_TRY(c, cudaMemcpy(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < kPhases; ++i) ts[i] = st.ts[i];
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_pingpong(nvrar_comm_t c, int peer, int iters, int initiator, void* stream,
+                   uint64_t* elapsed_ns) {
+  if (!c || !elapsed_ns || peer < 0 || peer >= c->world || peer == c->rank || iters < 1) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad pingpong argument");
+  }
+  if (!c->connected) return fail(c, NVRAR_ERR_NOT_CONNECTED, "comm not connected");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  LaunchParams lp{};
+  lp.d0 = c->h_desc;
+  lp.nlocal = 1;
+  const uint64_t base = c->pp_base;
+  c->pp_base += static_cast<uint64_t>(iters) + 1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  pingpong_fn()<<<1, 32, 0, s>>>(lp, peer, iters, base, initiator, c->d_scratch);
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  CUDA_TRY(c, cudaMemcpy(elapsed_ns, c->d_scratch, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (*elapsed_ns == ~0ull) return fail(c, NVRAR_ERR_DEADLOCK, "pingpong timed out");
   return NVRAR_SUCCESS;
 }
 

@@ -58,14 +58,19 @@ struct ErrRec {
 };
 
 // Private (not shared) per-rank state. seq is the NvrarAllreduce::seq_ analogue
-// (nvrar.hpp:248): the kernel reads seq+1 as its call number and the last CTA
-// to finish stores it back, so the counter stays on the device and a CUDA
-// graph of back-to-back calls needs no host involvement.
+// (nvrar.hpp:248): the kernel reads seq+1 as its call number and stores it
+// back on exit, so the counter stays on the device and a CUDA graph of
+// back-to-back calls needs no host involvement.
+constexpr int kSeqSlots = 512;  // >= co-resident CTAs of one launch
+constexpr int kPhases = 8;
+
+// seq is replicated in kSeqSlots slots: CTA b reads slot b at entry and, on
+// exit, writes slots b, b+grid, b+2*grid, ... — so every slot advances on every
+// call whatever the grid size, without atomics or a grid-wide barrier.
 struct RankState {
-  uint32_t seq;
-  uint32_t done;
-  uint32_t pad[2];
+  uint32_t seq[kSeqSlots];
   ErrRec err;
+  uint64_t ts[kPhases];  // phase timestamps of CTA 0, thread 0 (profiling)
 };
 
 struct RankDesc {
@@ -73,10 +78,15 @@ struct RankDesc {
   RankState* state;          // own
   Layout lay;
   int rank, world, nodes, gpus, steps, node, local;
+  int profile;
   uint64_t timeout_ns;
 };
 
+// One rank per launch (the real multi-GPU path) passes its descriptor BY VALUE
+// (__grid_constant__ param space: no dependent global loads in the prologue);
+// virtual ranks sharing a device (EMU) go through the pointer table.
 struct LaunchParams {
+  RankDesc d0;
   const RankDesc* desc[kMaxLocal];
   const void* send[kMaxLocal];
   void* recv[kMaxLocal];
@@ -132,7 +142,8 @@ __device__ __forceinline__ uint32_t ld_volatile32(const void* p) {
 // flow (so every __syncthreads is still reached) but stops waiting.
 
 struct Ctl {
-  const RankDesc* d;
+  RankState* st;
+  uint64_t timeout_ns;
   uint32_t seq;
   uint32_t spins;
   uint64_t t0;
@@ -141,7 +152,7 @@ struct Ctl {
 
 __device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, int peer,
                                              uint64_t word, uint64_t observed) {
-  ErrRec* e = &c.d->state->err;
+  ErrRec* e = &c.st->err;
   if (atomicCAS(&e->code, 0u, 0xFFFFFFFFu) == 0u) {
     e->kind = kind;
     e->peer = peer;
@@ -159,12 +170,12 @@ __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t w
                                           uint64_t observed) {
   if (c.aborted) return true;
   if ((++c.spins & 127u) != 0u) return false;
-  if (ld_volatile32(&c.d->state->err.code) != 0u) {
+  if (ld_volatile32(&c.st->err.code) != 0u) {
     c.aborted = true;
     return true;
   }
   const uint64_t now = globaltimer();
-  if (now - c.t0 > c.d->timeout_ns) {
+  if (now - c.t0 > c.timeout_ns) {
     record_fault(c, kDeadlock, kind, peer, word, observed);
     return true;
   }
@@ -387,6 +398,21 @@ __device__ __forceinline__ uint4* slot_c(const RankDesc& d, int rank, uint32_t p
 }
 __device__ __forceinline__ uint64_t* counters(const RankDesc& d, int rank) {
   return reinterpret_cast<uint64_t*>(d.base[rank] + d.lay.ctrl_off);
+}
+// ping-pong word (signal-latency probe), right after the counters
+__device__ __forceinline__ uint64_t* diag_word(const RankDesc& d, int rank) {
+  return counters(d, rank) + kMaxRanks;
+}
+
+// Programmatic dependent launch: everything before pdl_wait() may overlap the
+// previous kernel on the stream; nothing it wrote may be touched before.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ void stamp(const RankDesc& d, int k) {
+  if (d.profile && blockIdx.x == 0 && threadIdx.x == 0) d.state->ts[k] = globaltimer();
 }
 
 }  // namespace nvrar

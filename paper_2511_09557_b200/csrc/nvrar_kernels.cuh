@@ -1,4 +1,5 @@
-// B200 (sm_100a) kernels of the NVRAR all-reduce.
+// B200 (sm_100a) kernels of the NVRAR all-reduce (templates; instantiated per
+// dtype in nvrar_inst_*.cu so the build compiles them in parallel).
 //
 // One persistent launch per call runs every phase of the schedule; no host
 // round trip, no NCCL. Two kernel families compute the SAME bits — the
@@ -36,11 +37,50 @@
 // (nvrar.hpp:107-109,124-126). A rank can only write parity p again in call
 // k+2 after finishing call k+1, which needed data the reader sent only after
 // it had finished call k — so a slot is never overwritten before it is read.
+#pragma once
+
 #include <cuda_runtime.h>
 
 #include "nvrar_device.cuh"
 
 namespace nvrar {
+
+template <bool EMU>
+__device__ __forceinline__ const RankDesc& rank_desc(const LaunchParams& lp) {
+  if constexpr (EMU) {
+    return *lp.desc[blockIdx.y];
+  } else {
+    return lp.d0;
+  }
+}
+
+// Prologue. Returns false when the communicator carries a sticky fault.
+__device__ __forceinline__ bool begin_call(const RankDesc& d, Ctl& c) {
+  __shared__ uint32_t s_seq, s_err;
+  stamp(d, 0);
+  pdl_wait();  // the previous call (and the producer of our input) is complete
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    s_err = ld_volatile32(&d.state->err.code);
+    s_seq = ld_volatile32(&d.state->seq[blockIdx.x]);
+  }
+  __syncthreads();
+  c.st = d.state;
+  c.timeout_ns = d.timeout_ns;
+  c.spins = 0;
+  c.aborted = false;
+  c.t0 = globaltimer();
+  c.seq = s_seq + 1u;
+  stamp(d, 1);
+  return s_err == 0u;
+}
+
+__device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
+  if (threadIdx.x == 0) {
+    for (int i = blockIdx.x; i < kSeqSlots; i += gridDim.x) d.state->seq[i] = seq;
+  }
+  stamp(d, 6);
+}
 
 __device__ __forceinline__ void publish_seq_len(const RankDesc& d, int peer, uint32_t seq,
                                                 uint64_t n) {
@@ -66,19 +106,6 @@ __device__ __forceinline__ void wait_seq_len(Ctl& c, const RankDesc& d, int peer
   }
 }
 
-__device__ __forceinline__ void finish_call(const RankDesc& d, uint32_t seq) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    RankState* st = d.state;
-    if (atomicAdd(&st->done, 1u) == gridDim.x - 1) {
-      st->done = 0;
-      st->seq = seq;
-      __threadfence();
-    }
-  }
-}
-
 template <int N>
 struct Log2 {
   static constexpr int value = N <= 1 ? 0 : 1 + Log2<N / 2>::value;
@@ -100,19 +127,14 @@ constexpr int kHierMaxG = 8;
 constexpr int kHierUpt = 2;  // units per thread carried through the RD steps together
 
 // ---------------------------------------------------------------------------
-template <class E, int N>
+template <class E, int N, bool EMU>
 __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
   constexpr int DW = E::DW;
   constexpr int kSteps = Log2<N>::value;
-  const RankDesc& d = *lp.desc[blockIdx.y];
+  const RankDesc& d = rank_desc<EMU>(lp);
   Ctl c;
-  c.d = &d;
-  c.spins = 0;
-  c.aborted = false;
-  if (ld_volatile32(&d.state->err.code) != 0u) return;  // sticky fault: comm is dead
-  c.t0 = globaltimer();
-  c.seq = ld_volatile32(&d.state->seq) + 1u;
+  if (!begin_call(d, c)) return;  // sticky fault: comm is dead
   const uint32_t parity = c.seq & 1u;
 
   const uint64_t n = lp.count;
@@ -121,8 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   const uint64_t U = (S + kUnit - 1) / kUnit;
   const uint64_t ub = U * blockIdx.x / gridDim.x;
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
-  const void* send = lp.send[blockIdx.y];
-  void* recv = lp.recv[blockIdx.y];
+  const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
+  void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
 
   // Peer-only sync, publish half (nvrar.hpp:163-171).
   if (kSteps > 0 && blockIdx.x == 0 && threadIdx.x < kSteps) {
@@ -136,15 +158,15 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       uint4* slot = slot_a(d, node * G + cc, parity, local);
       const uint64_t cbase = static_cast<uint64_t>(cc) * S;
       for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-        const uint64_t e = cbase + kUnit * u;
         const int valid = chunk_valid(S, u, n, cbase);
         if (valid == 0) continue;  // pure padding: skipped identically by the reader
         uint32_t raw[DW];
-        load_raw<E>(send, e, valid, raw);
+        load_raw<E>(send, cbase + kUnit * u, valid, raw);
         ll_store<DW>(slot, u, raw, c.seq);
       }
     }
   }
+  stamp(d, 2);
 
   // Peer-only sync, wait half: all log2(N) XOR peers before any RD send.
   if (kSteps > 0) {
@@ -153,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
     __syncthreads();
   }
+  stamp(d, 3);
 
   // Phases 1b+2+3a: fold own chunk, recursive doubling, cast + all-gather push.
   const uint64_t mybase = static_cast<uint64_t>(local) * S;
@@ -243,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       }
     }
   }
+  stamp(d, 4);
 
   // Phase 3b: all-gather receive.
   if (G > 1) {
@@ -272,8 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       }
     }
   }
-
-  finish_call(d, c.seq);
+  stamp(d, 5);
+  end_call(d, c.seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -298,18 +322,13 @@ __device__ __forceinline__ typename E::acc pick(const uint32_t (&r)[N][MAXG][E::
   return v;
 }
 
-template <class E, int N, int MAXG>
+template <class E, int N, int MAXG, bool EMU>
 __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
   constexpr int DW = E::DW;
-  const RankDesc& d = *lp.desc[blockIdx.y];
+  const RankDesc& d = rank_desc<EMU>(lp);
   Ctl c;
-  c.d = &d;
-  c.spins = 0;
-  c.aborted = false;
-  if (ld_volatile32(&d.state->err.code) != 0u) return;
-  c.t0 = globaltimer();
-  c.seq = ld_volatile32(&d.state->seq) + 1u;
+  if (!begin_call(d, c)) return;
   const uint32_t parity = c.seq & 1u;
 
   const uint64_t n = lp.count;
@@ -320,8 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const uint64_t U = SP / kUnit;
   const uint64_t ub = U * blockIdx.x / gridDim.x;
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
-  const void* send = lp.send[blockIdx.y];
-  void* recv = lp.recv[blockIdx.y];
+  const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
+  void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
 
   if (blockIdx.x == 0) {
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
@@ -343,11 +362,13 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       ll_store<DW>(slot, u, raw, c.seq);
     }
   }
+  stamp(d, 2);
 
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
     if (p != me) wait_seq_len(c, d, p, n);
   }
   __syncthreads();
+  stamp(d, 3);
 
   const uint64_t mybase = oneshot ? 0 : static_cast<uint64_t>(me) * SP;
   for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
@@ -436,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       for (int j = 1; j < P; ++j) ll_store<DW>(slot_b(d, (me + j) % P, parity, me), u, o, c.seq);
     }
   }
+  stamp(d, 4);
 
   if (!oneshot) {
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
@@ -450,61 +472,42 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       }
     }
   }
-
-  finish_call(d, c.seq);
+  stamp(d, 5);
+  end_call(d, c.seq);
 }
-
-__global__ void seq_bump_kernel(const __grid_constant__ LaunchParams lp) {
-  const RankDesc& d = *lp.desc[blockIdx.y];
-  if (threadIdx.x == 0 && ld_volatile32(&d.state->err.code) == 0u) d.state->seq += 1u;
-}
-
-// ---------------------------------------------------------------------------
-// Dispatch
 
 using KernelFn = void (*)(LaunchParams);
 
-template <class E>
+template <class E, bool EMU>
 KernelFn hier_for(int nodes) {
   switch (nodes) {
-    case 1: return hier_kernel<E, 1>;
-    case 2: return hier_kernel<E, 2>;
-    case 4: return hier_kernel<E, 4>;
-    case 8: return hier_kernel<E, 8>;
+    case 1: return hier_kernel<E, 1, EMU>;
+    case 2: return hier_kernel<E, 2, EMU>;
+    case 4: return hier_kernel<E, 4, EMU>;
+    case 8: return hier_kernel<E, 8, EMU>;
+    default: return nullptr;
+  }
+}
+
+template <class E, bool EMU>
+KernelFn flat_for(int nodes) {
+  switch (nodes) {
+    case 1: return flat_kernel<E, 1, 8, EMU>;
+    case 2: return flat_kernel<E, 2, 8, EMU>;
+    case 4: return flat_kernel<E, 4, 4, EMU>;
+    case 8: return flat_kernel<E, 8, 2, EMU>;
     default: return nullptr;
   }
 }
 
 template <class E>
-KernelFn flat_for(int nodes) {
-  switch (nodes) {
-    case 1: return flat_kernel<E, 1, 8>;
-    case 2: return flat_kernel<E, 2, 8>;
-    case 4: return flat_kernel<E, 4, 4>;
-    case 8: return flat_kernel<E, 8, 2>;
-    default: return nullptr;
-  }
+KernelFn kernel_for(bool flat, int nodes, bool emu) {
+  if (flat) return emu ? flat_for<E, true>(nodes) : flat_for<E, false>(nodes);
+  return emu ? hier_for<E, true>(nodes) : hier_for<E, false>(nodes);
 }
 
-int flat_max_gpus(int nodes) {
-  switch (nodes) {
-    case 1: return 8;
-    case 2: return 8;
-    case 4: return 4;
-    case 8: return 2;
-    default: return 0;
-  }
-}
-
-KernelFn select_kernel(int dtype, bool flat, int nodes) {
-  switch (dtype) {
-    case 0: return flat ? flat_for<I32>(nodes) : hier_for<I32>(nodes);
-    case 1: return flat ? flat_for<F32>(nodes) : hier_for<F32>(nodes);
-    case 2: return flat ? flat_for<BF16>(nodes) : hier_for<BF16>(nodes);
-    default: return nullptr;
-  }
-}
-
-KernelFn bump_kernel() { return seq_bump_kernel; }
+KernelFn kernel_f32(bool flat, int nodes, bool emu);
+KernelFn kernel_bf16(bool flat, int nodes, bool emu);
+KernelFn kernel_i32(bool flat, int nodes, bool emu);
 
 }  // namespace nvrar
