@@ -1,0 +1,121 @@
+// Reference-side binding: a drop-in for ccsim::NvrarAllreduce<T>
+// (/root/reference/proj/include/ccsim/collectives/nvrar.hpp:41-250) that runs
+// the all-reduce on B200s through the C ABI in include/nvrar.h.
+//
+// This is the header a maintainer of the reference would add next to
+// collectives/nvrar.hpp. It keeps the reference's names, argument meaning and
+// exception types (errors.hpp); the transport context (Ctx) is replaced by
+// real GPUs: one process per GPU, a bootstrap allgather supplied by the host
+// program (MPI, torch.distributed, a file store...).
+//
+// Differences a caller must know:
+//  * buffers are DEVICE pointers (std::span over device memory), and run() is
+//    stream-ordered; run() synchronises the stream and checks the device
+//    status so that faults surface as the reference's exceptions;
+//  * the DeadlockError blocked set carries this rank's entry only (each
+//    process sees its own watchdog record); the all-ranks view is
+//    LocalGroup.check() on one device or a host-side gather.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ccsim/collectives/fused.hpp"  // Element, NvrarConfig
+#include "ccsim/errors.hpp"
+#include "ccsim/topology.hpp"
+#include "nvrar.h"
+
+namespace ccsim {
+
+template <Element T>
+class NvrarB200Allreduce {
+ public:
+  using Allgather = nvrar_allgather_fn;
+
+  NvrarB200Allreduce(const ClusterTopology& topo, int rank, int device, std::size_t max_elems,
+                     Allgather allgather, void* allgather_ctx, double timeout_s = 5.0)
+      : max_elems_(max_elems) {
+    topo.require_power_of_two_nodes("nvrar");  // InvalidTopologyError, nvrar.hpp:46
+    nvrar_init_args a{};
+    a.world_size = topo.world_size();
+    a.rank = rank;
+    a.nodes = topo.nodes;
+    a.gpus_per_node = topo.gpus_per_node;
+    a.device = device;
+    a.max_bytes = std::max<std::size_t>(max_elems, 1) * sizeof(T);
+    a.timeout_s = timeout_s;
+    a.allgather = allgather;
+    a.allgather_ctx = allgather_ctx;
+    throw_on(nvrar_init(&a, &comm_), nullptr);
+  }
+  NvrarB200Allreduce(const NvrarB200Allreduce&) = delete;
+  NvrarB200Allreduce& operator=(const NvrarB200Allreduce&) = delete;
+  ~NvrarB200Allreduce() { nvrar_finalize(comm_); }
+
+  std::uint32_t sequence() const {
+    std::uint32_t s = 0;
+    throw_on(nvrar_get_sequence(comm_, &s), comm_);
+    return s;
+  }
+
+  /// Same contract as NvrarAllreduce<T>::run (nvrar.hpp:84-129), on device memory.
+  void run(std::span<const T> in, std::span<T> out, const NvrarConfig& cfg = {},
+           void* stream = nullptr) {
+    cfg.validate();
+    if (in.size() != out.size()) {
+      throw InvalidArgumentError("nvrar: input and output lengths differ");
+    }
+    if (in.size() > max_elems_) {
+      throw InvalidArgumentError("nvrar: vector longer than the preallocated maximum");
+    }
+    throw_on(nvrar_set_config(comm_, cfg.blocks, cfg.chunk_bytes), comm_);
+    throw_on(nvrar_allreduce(comm_, in.data(), out.data(), in.size(), dtype(), NVRAR_SUM, stream),
+             comm_);
+    throw_on(nvrar_check(comm_), comm_);  // synchronises; device faults -> exceptions
+  }
+
+  /// Step-l exchange peers (nvrar.hpp:158).
+  std::vector<RankId> peers(const ClusterTopology& topo) const {
+    int p[8];
+    int steps = 0;
+    throw_on(nvrar_get_peers(comm_, p, 8, &steps), comm_);
+    std::vector<RankId> out;
+    for (int l = 0; l < steps; ++l) out.push_back(RankId::from_global(p[l], topo));
+    return out;
+  }
+
+ private:
+  static constexpr nvrar_dtype_t dtype() {
+    return std::same_as<T, float> ? NVRAR_FLOAT32 : NVRAR_INT32;
+  }
+
+  static void throw_on(int rc, nvrar_comm_t comm) {
+    if (rc == NVRAR_SUCCESS) return;
+    const std::string msg = nvrar_last_error(comm);
+    switch (rc) {
+      case NVRAR_ERR_INVALID_ARGUMENT: throw InvalidArgumentError(msg);
+      case NVRAR_ERR_INVALID_TOPOLOGY: throw InvalidTopologyError(msg);
+      case NVRAR_ERR_PROTOCOL_FAULT: throw ProtocolFaultError(msg);
+      case NVRAR_ERR_DEADLOCK: {
+        nvrar_blocked_t b{};
+        nvrar_get_blocked(comm, &b);
+        BlockedRank br;
+        br.global_rank = b.global_rank;
+        br.kind = b.kind == 1 ? BlockedRank::Kind::SeqWait : BlockedRank::Kind::FlagWait;
+        br.peer_rank = b.peer_rank;
+        br.word_index = b.word_index;
+        br.expected = b.expected;
+        throw DeadlockError({br});
+      }
+      default: throw std::runtime_error("nvrar: " + msg);
+    }
+  }
+
+  nvrar_comm_t comm_ = nullptr;
+  std::size_t max_elems_;
+};
+
+}  // namespace ccsim
