@@ -88,6 +88,15 @@ typedef enum {
   NVRAR_ALGO_ONESHOT = 3
 } nvrar_algo_t;
 
+/* Wire protocol. Both are self-validating (arrival of data = arrival of its
+ * signal) and give identical results:
+ *   LL      — the reference's fused word: 4-byte payload + 4-byte sequence flag
+ *             per 8 bytes (fused.hpp:4-8); 2x wire bytes. Always used for int32.
+ *   LAMPORT — raw payload (1x wire bytes); the all-ones bit pattern (a NaN) marks
+ *             "not arrived", and an all-ones NaN input travels as another NaN.
+ *   AUTO    — LAMPORT for float32/bf16, LL for int32. */
+typedef enum { NVRAR_PROTO_AUTO = 0, NVRAR_PROTO_LL = 1, NVRAR_PROTO_LAMPORT = 2 } nvrar_proto_t;
+
 /* Bootstrap collective supplied by the caller for nvrar_init: gather `bytes`
  * from every rank into recv (rank-major). Return 0 on success. */
 typedef int (*nvrar_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
@@ -152,6 +161,7 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
 int nvrar_set_config(nvrar_comm_t comm, int blocks, uint64_t chunk_bytes);
 int nvrar_set_algo(nvrar_comm_t comm, nvrar_algo_t algo);
 int nvrar_set_timeout(nvrar_comm_t comm, double timeout_s);
+int nvrar_set_protocol(nvrar_comm_t comm, nvrar_proto_t proto);
 /* Selected schedule and CTA count for a message (what nvrar_allreduce runs). */
 int nvrar_plan(nvrar_comm_t comm, size_t count, nvrar_dtype_t dtype, int* algo, int* blocks);
 /* The same selector as a pure function (no device): every rank evaluates it

@@ -28,6 +28,9 @@ ALGO_AUTO, ALGO_HIER, ALGO_TWOSHOT, ALGO_ONESHOT = 0, 1, 2, 3
 ALGO_NAMES = {ALGO_AUTO: "auto", ALGO_HIER: "hier", ALGO_TWOSHOT: "twoshot",
               ALGO_ONESHOT: "oneshot"}
 
+PROTO_AUTO, PROTO_LL, PROTO_LAMPORT = 0, 1, 2
+PROTO_CODES = {"auto": PROTO_AUTO, "ll": PROTO_LL, "lamport": PROTO_LAMPORT}
+
 HANDLE_BYTES = 256
 MAX_LOCAL = 32
 
@@ -84,6 +87,7 @@ SIGNATURES = {
     "nvrar_set_config": (_c.c_int, [_vp, _c.c_int, _c.c_uint64]),
     "nvrar_set_algo": (_c.c_int, [_vp, _c.c_int]),
     "nvrar_set_timeout": (_c.c_int, [_vp, _c.c_double]),
+    "nvrar_set_protocol": (_c.c_int, [_vp, _c.c_int]),
     "nvrar_plan": (_c.c_int, [_vp, _c.c_size_t, _c.c_int, _c.POINTER(_c.c_int),
                               _c.POINTER(_c.c_int)]),
     "nvrar_plan_for": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_size_t, _c.c_int, _c.c_int,

@@ -248,6 +248,10 @@ class Communicator:
     def set_timeout(self, seconds: float) -> None:
         self._check(self._lib.nvrar_set_timeout(self._h, seconds))
 
+    def set_protocol(self, proto: str) -> None:
+        """'auto' | 'll' (fused seq words, as the reference) | 'lamport' (raw payload)."""
+        self._check(self._lib.nvrar_set_protocol(self._h, L.PROTO_CODES[proto]))
+
     def plan(self, count: int, dtype: torch.dtype):
         a, b = ctypes.c_int(), ctypes.c_int()
         self._check(self._lib.nvrar_plan(self._h, count, dtype_code(dtype), ctypes.byref(a),
@@ -402,6 +406,10 @@ class LocalGroup:
     def set_timeout(self, s: float) -> None:
         for c in self.comms:
             c.set_timeout(s)
+
+    def set_protocol(self, proto: str) -> None:
+        for c in self.comms:
+            c.set_protocol(proto)
 
     def launch(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
                active: Optional[Sequence[int]] = None,

@@ -18,7 +18,7 @@
 
 namespace nvrar {
 using KernelFn = void (*)(LaunchParams);
-KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu);
+KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu, bool lamport);
 KernelFn bump_kernel();
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);
 PingFn pingpong_fn();
@@ -57,7 +57,6 @@ bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
 size_t dtype_bytes(int dt) { return dt == NVRAR_BF16 ? 2 : 4; }
 
-uint64_t units_for(uint64_t elems) { return (elems + kUnit - 1) / kUnit + 1; }
 
 }  // namespace
 
@@ -80,7 +79,8 @@ struct nvrar_comm {
   std::string last_error;
   int max_ctas = 148;  // co-resident CTAs of one kernel on this device
   bool pdl = true;     // programmatic dependent launch for single-rank launches
-  uint64_t pp_base = 0;
+  int proto = NVRAR_PROTO_AUTO;
+  uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
   uint64_t* d_scratch = nullptr;
 };
 
@@ -111,10 +111,12 @@ int fail(nvrar_comm* c, int code, const char* fmt, ...) {
 
 Layout make_layout(int world, int nodes, int gpus, size_t max_bytes) {
   // Sized for the worst dtype (bf16: most elements per byte) and every schedule.
-  const uint64_t max_elems = std::max<uint64_t>(max_bytes / 2, 4);
-  const uint64_t ug = units_for((max_elems + gpus - 1) / gpus);
-  const uint64_t up = units_for((max_elems + world - 1) / world + 3);
-  const uint64_t u1 = units_for(std::min<uint64_t>(max_elems, kOneshotMaxBytes / 2));
+  // Worst wire cost is 8 bytes per element (LL words / LL fp32 partials), and
+  // a unit holds at most 8 elements; slots round up to 32-unit groups.
+  const uint64_t max_elems = std::max<uint64_t>(max_bytes / 2, 8);
+  const uint64_t eg = (max_elems + gpus - 1) / gpus;
+  const uint64_t ep = (max_elems + world - 1) / world + 8;
+  const uint64_t e1 = std::min<uint64_t>(max_elems, kOneshotMaxBytes / 2) + 8;
   const int steps = log2_exact(nodes);
   Layout l{};
   uint64_t off = 0;
@@ -124,13 +126,14 @@ Layout make_layout(int world, int nodes, int gpus, size_t max_bytes) {
     return o;
   };
   l.ctrl_off = take(sizeof(uint64_t) * kMaxRanks);
-  // 4 LL words (32 B) per unit; 32-unit groups so round up to 32 units.
-  auto slot_words = [](uint64_t units) { return ((units + 31) & ~31ull) * 4; };
-  l.a_src = slot_words(std::max({gpus > 1 ? ug : 0, up, u1}));
+  // 8-byte words per slot: one per element (8 B/element worst) rounded up to
+  // whole 32-unit groups of up to 8 elements.
+  auto slot_words = [](uint64_t elems) { return ((elems + 255) & ~255ull) + 256; };
+  l.a_src = slot_words(std::max({gpus > 1 ? eg : 0, ep, e1}));
   l.a_off = take(2ull * world * l.a_src * 8);
-  l.b_src = slot_words(std::max(gpus > 1 ? ug : 0, up));
+  l.b_src = slot_words(std::max(gpus > 1 ? eg : 0, ep));
   l.b_off = take(2ull * world * l.b_src * 8);
-  l.c_step = slot_words(ug);
+  l.c_step = slot_words(eg);
   l.c_off = take(2ull * std::max(steps, 1) * l.c_step * 8);
   l.bytes = off;
   return l;
@@ -271,7 +274,8 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
     return cleanup(NVRAR_ERR_CUDA);
   }
   if ((e = cudaMalloc(&c->region, c->lay.bytes)) != cudaSuccess ||
-      (e = cudaMemset(c->region, 0, c->lay.bytes)) != cudaSuccess ||
+      // all-ones = empty cell for both wire protocols (and a counter no seq matches)
+      (e = cudaMemset(c->region, 0xFF, c->lay.bytes)) != cudaSuccess ||
       (e = cudaMalloc(&c->state, sizeof(RankState))) != cudaSuccess ||
       (e = cudaMemset(c->state, 0, sizeof(RankState))) != cudaSuccess ||
       (e = cudaMalloc(&c->d_desc, sizeof(RankDesc))) != cudaSuccess ||
@@ -288,7 +292,7 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
       for (int emu = 0; emu < 2; ++emu) {
         int o = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &o, reinterpret_cast<const void*>(select_kernel(dt, flat, c->nodes, emu)),
+                &o, reinterpret_cast<const void*>(select_kernel(dt, flat, c->nodes, emu, true)),
                 kThreads, 0) == cudaSuccess &&
             o > 0) {
           occ = flat + dt + emu == 0 ? o : std::min(occ, o);
@@ -298,6 +302,10 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   }
   c->max_ctas = std::max(1, std::min(kSeqSlots, sms * std::max(occ, 1)));
   if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
+  if (const char* v = getenv("NVRAR_PROTO")) {
+    c->proto = std::string(v) == "ll" ? NVRAR_PROTO_LL
+               : std::string(v) == "lamport" ? NVRAR_PROTO_LAMPORT : NVRAR_PROTO_AUTO;
+  }
   c->h_desc = RankDesc{};
   c->h_desc.state = c->state;
   c->h_desc.lay = c->lay;
@@ -465,6 +473,14 @@ int nvrar_set_algo(nvrar_comm_t c, nvrar_algo_t algo) {
   return NVRAR_SUCCESS;
 }
 
+int nvrar_set_protocol(nvrar_comm_t c, nvrar_proto_t proto) {
+  if (!c || proto < NVRAR_PROTO_AUTO || proto > NVRAR_PROTO_LAMPORT) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad protocol");
+  }
+  c->proto = proto;
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_set_timeout(nvrar_comm_t c, double timeout_s) {
   if (!c || !(timeout_s > 0)) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad timeout");
   c->timeout_s = timeout_s;
@@ -549,7 +565,8 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
   if (!emu) lp.d0 = c0->h_desc;  // by value: the kernel reads it from param space
-  KernelFn k = select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu);
+  const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
+  KernelFn k = select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu, lamport);
   if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
 
   cudaLaunchConfig_t cfg{};
@@ -631,8 +648,10 @@ int nvrar_pingpong(nvrar_comm_t c, int peer, int iters, int initiator, void* str
   LaunchParams lp{};
   lp.d0 = c->h_desc;
   lp.nlocal = 1;
-  const uint64_t base = c->pp_base;
-  c->pp_base += static_cast<uint64_t>(iters) + 1;
+  // values unique per (pair, call): a stale echo from another pair never matches
+  const int lo = std::min(peer, c->rank), hi = std::max(peer, c->rank);
+  const uint64_t base = (static_cast<uint64_t>(lo * kMaxRanks + hi + 1) << 40) + c->pp_base[peer];
+  c->pp_base[peer] += static_cast<uint64_t>(iters) + 1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   pingpong_fn()<<<1, 32, 0, s>>>(lp, peer, iters, base, initiator, c->d_scratch);
   CUDA_TRY(c, cudaGetLastError());

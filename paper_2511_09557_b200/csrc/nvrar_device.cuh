@@ -1,16 +1,23 @@
 // Device-side data structures and primitives of the B200 NVRAR all-reduce.
 //
 // Transport model (replaces the reference's one-sided Ctx, transport.hpp:137-202):
-//  * every rank owns ONE symmetric region (same layout on all ranks, zeroed at
-//    creation, mapped into each peer process through CUDA IPC) — the analogue
-//    of Ctx::alloc_region's symmetric, zero-filled regions;
-//  * data moves as LL ("low-latency") words: 8 bytes = 4-byte payload (low) +
-//    4-byte sequence flag (high), i.e. the reference's fused word
-//    (transport.hpp:81-87, fused.hpp:4-8). A thread stores two words with one
-//    16-byte st.volatile over NVLink and the receiver polls the words
-//    themselves, so arrival of data is arrival of its signal — no fence and no
-//    per-pair ordering assumption (NVLink does not order weak stores to
-//    different addresses, unlike the reference transport, transport.hpp:9-11);
+//  * every rank owns ONE symmetric region (same layout on all ranks, mapped
+//    into each peer process through CUDA IPC) — the analogue of
+//    Ctx::alloc_region's symmetric regions;
+//  * slots are arrays of 16-byte cells. A cell is EMPTY when all its bits are
+//    ones; the region starts empty and every reader re-empties what it read,
+//    so the invariant holds between calls whatever protocol used the slot;
+//  * two wire protocols, both self-validating (arrival of data is arrival of
+//    its signal — no fence, no per-pair ordering assumption; NVLink does not
+//    order weak stores to different addresses, unlike the reference
+//    transport, transport.hpp:9-11):
+//      LL      — the reference's fused word (transport.hpp:81-87, fused.hpp:4-8):
+//                8 bytes = 4-byte payload (low) + 4-byte sequence flag (high);
+//                eta = 2. Used for int32 (no spare bit pattern) and on request.
+//      Lamport — raw payload (eta = 1); the all-ones pattern (a NaN in fp32
+//                and bf16) means "not arrived", writers map that one NaN
+//                pattern to another NaN. Default for fp32 / bf16.
+//    Both are double-buffered by call parity (nvrar.hpp:107-109,124-126).
 //  * sequence/length words (seq<<32 | len) published into the peer's counter
 //    array stand in for Ctx::publish_counter (transport.hpp:161-164), and the
 //    wait on them is the reference's peer-only sync (nvrar.hpp:163-171).
@@ -23,7 +30,6 @@ namespace nvrar {
 constexpr int kMaxRanks = 64;   // NVRAR_MAX_RANKS
 constexpr int kMaxLocal = 32;   // NVRAR_MAX_LOCAL (virtual ranks per launch)
 constexpr int kThreads = 512;   // threads per CTA
-constexpr int kUnit = 4;        // elements per unit (one thread's work item)
 
 enum Status : uint32_t {
   kOk = 0,
@@ -53,7 +59,7 @@ struct ErrRec {
   int32_t kind;       // WaitKind
   int32_t peer;       // global rank awaited
   uint32_t expected;  // awaited sequence number
-  uint64_t word;      // word index inside the awaited slot (FlagWait)
+  uint64_t word;      // unit index inside the awaited slot (FlagWait)
   uint64_t observed;  // what was seen instead
 };
 
@@ -182,106 +188,158 @@ __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t w
   return false;
 }
 
-// flag observed in a slot for call `seq`: equal = arrived; behind = not yet;
-// ahead = a peer ran more calls than this rank (ProtocolFaultError).
+// flag observed in a slot for call `seq`: equal = arrived; behind = not yet
+// (an empty cell reads 0xFFFFFFFF); ahead = a peer ran more calls than this
+// rank (ProtocolFaultError).
 __device__ __forceinline__ bool flag_ahead(uint32_t flag, uint32_t seq) {
-  return static_cast<int32_t>(flag - seq) > 0;
+  return flag != 0xFFFFFFFFu && static_cast<int32_t>(flag - seq) > 0;
 }
 
 // ---------------------------------------------------------------------------
-// LL slots. A unit carries DW payload dwords as DW LL words (DW/2 16-byte
-// stores). Within each group of 32 units, part h of all 32 units is
+// Wire protocols over 16-byte cells. A unit carries W payload dwords in
+// cells<W>() cells; within each group of 32 units, cell h of all 32 units is
 // contiguous, so one warp-wide store writes 512 contiguous bytes.
 
-template <int DW>
-__device__ __forceinline__ uint64_t ll_off16(uint64_t u, int h) {
-  return (((u >> 5) * (DW / 2) + static_cast<uint64_t>(h)) << 5) + (u & 31);
+__device__ __forceinline__ uint64_t cell_index(uint64_t u, int cells, int h) {
+  return (((u >> 5) * static_cast<uint64_t>(cells) + static_cast<uint64_t>(h)) << 5) + (u & 31);
 }
 
-template <int DW>
-__device__ __forceinline__ void ll_store(uint4* slot, uint64_t u, const uint32_t (&d)[DW],
-                                         uint32_t seq) {
-#pragma unroll
-  for (int h = 0; h < DW / 2; ++h) {
-    st_volatile16(slot + ll_off16<DW>(u, h), d[2 * h], seq, d[2 * h + 1], seq);
+struct LL {
+  static constexpr bool kLamport = false;
+  template <int W>
+  static constexpr int cells() {
+    return W / 2;
   }
-}
-
-// One non-blocking attempt: fills d and returns true when every word carries
-// `seq`.
-template <int DW>
-__device__ __forceinline__ bool ll_try(const uint4* slot, uint64_t u, uint32_t seq,
-                                       uint32_t (&d)[DW], uint32_t& bad_flag) {
-  bool ok = true;
+  template <int W>
+  __device__ static __forceinline__ void put(uint4* slot, uint64_t u, const uint32_t (&d)[W],
+                                             uint32_t seq) {
 #pragma unroll
-  for (int h = 0; h < DW / 2; ++h) {
-    const uint4 v = ld_volatile16(slot + ll_off16<DW>(u, h));
-    d[2 * h] = v.x;
-    d[2 * h + 1] = v.z;
-    if (v.y != seq) {
-      ok = false;
-      bad_flag = v.y;
-    }
-    if (v.w != seq) {
-      ok = false;
-      bad_flag = v.w;
+    for (int h = 0; h < W / 2; ++h) {
+      st_volatile16(slot + cell_index(u, W / 2, h), d[2 * h], seq, d[2 * h + 1], seq);
     }
   }
-  return ok;
-}
+  template <int W>
+  __device__ static __forceinline__ bool try_get(const uint4* slot, uint64_t u, uint32_t seq,
+                                                 uint32_t (&d)[W], uint32_t& bad) {
+    bool ok = true;
+#pragma unroll
+    for (int h = 0; h < W / 2; ++h) {
+      const uint4 v = ld_volatile16(slot + cell_index(u, W / 2, h));
+      d[2 * h] = v.x;
+      d[2 * h + 1] = v.z;
+      if (v.y != seq) {
+        ok = false;
+        bad = v.y;
+      }
+      if (v.w != seq) {
+        ok = false;
+        bad = v.w;
+      }
+    }
+    return ok;
+  }
+  template <int W>
+  __device__ static __forceinline__ void clear(uint4* slot, uint64_t u) {
+#pragma unroll
+    for (int h = 0; h < W / 2; ++h) {
+      st_volatile16(slot + cell_index(u, W / 2, h), ~0u, ~0u, ~0u, ~0u);
+    }
+  }
+};
 
-// Blocking poll with watchdog. `peer` labels the diagnosis.
-template <int DW>
-__device__ __forceinline__ void ll_wait(Ctl& c, const uint4* slot, uint64_t u,
-                                        uint32_t (&d)[DW], int peer) {
+// EB = element width in bytes for the sentinel test (2 = bf16, 4 = fp32).
+template <int EB>
+struct Lamport {
+  static constexpr bool kLamport = true;
+  template <int W>
+  static constexpr int cells() {
+    return W / 4;
+  }
+  // An all-ones element is the only pattern a writer may never send.
+  __device__ static __forceinline__ uint32_t canon(uint32_t x) {
+    if constexpr (EB == 4) {
+      return x == 0xFFFFFFFFu ? 0x7FFFFFFFu : x;
+    } else {
+      const uint32_t m = __vcmpeq2(x, 0xFFFFFFFFu);  // 0xFFFF per all-ones half
+      return x ^ (m & 0x80008000u);                  // -> 0x7FFF (another NaN)
+    }
+  }
+  __device__ static __forceinline__ bool empty(uint32_t x) {
+    if constexpr (EB == 4) {
+      return x == 0xFFFFFFFFu;
+    } else {
+      return __vcmpeq2(x, 0xFFFFFFFFu) != 0u;
+    }
+  }
+  template <int W>
+  __device__ static __forceinline__ void put(uint4* slot, uint64_t u, const uint32_t (&d)[W],
+                                             uint32_t) {
+#pragma unroll
+    for (int h = 0; h < W / 4; ++h) {
+      st_volatile16(slot + cell_index(u, W / 4, h), canon(d[4 * h]), canon(d[4 * h + 1]),
+                    canon(d[4 * h + 2]), canon(d[4 * h + 3]));
+    }
+  }
+  template <int W>
+  __device__ static __forceinline__ bool try_get(const uint4* slot, uint64_t u, uint32_t,
+                                                 uint32_t (&d)[W], uint32_t& bad) {
+    bool ok = true;
+#pragma unroll
+    for (int h = 0; h < W / 4; ++h) {
+      const uint4 v = ld_volatile16(slot + cell_index(u, W / 4, h));
+      d[4 * h] = v.x;
+      d[4 * h + 1] = v.y;
+      d[4 * h + 2] = v.z;
+      d[4 * h + 3] = v.w;
+      if (empty(v.x) || empty(v.y) || empty(v.z) || empty(v.w)) ok = false;
+    }
+    bad = 0xFFFFFFFFu;
+    return ok;
+  }
+  template <int W>
+  __device__ static __forceinline__ void clear(uint4* slot, uint64_t u) {
+#pragma unroll
+    for (int h = 0; h < W / 4; ++h) {
+      st_volatile16(slot + cell_index(u, W / 4, h), ~0u, ~0u, ~0u, ~0u);
+    }
+  }
+};
+
+// Blocking receive of unit u with watchdog; the cells are re-emptied after the
+// read. `peer` labels the diagnosis.
+template <class Pr, int W>
+__device__ __forceinline__ void recv_unit(Ctl& c, uint4* slot, uint64_t u, uint32_t (&d)[W],
+                                          int peer) {
   uint32_t bad = 0;
-  while (!ll_try<DW>(slot, u, c.seq, d, bad)) {
-    if (flag_ahead(bad, c.seq)) {
-      record_fault(c, kProtocolFault, kStaleFlag, peer, u * DW, bad);
+  while (!Pr::template try_get<W>(slot, u, c.seq, d, bad)) {
+    if (!Pr::kLamport && flag_ahead(bad, c.seq)) {
+      record_fault(c, kProtocolFault, kStaleFlag, peer, u, bad);
       return;
     }
-    if (wait_tick(c, kFlagWait, peer, u * DW, bad)) return;
+    if (wait_tick(c, kFlagWait, peer, u, bad)) return;
   }
+  Pr::template clear<W>(slot, u);
 }
 
 // ---------------------------------------------------------------------------
-// Element traits. A unit is kUnit=4 elements; RAW is the caller dtype's bits,
-// ACC the arithmetic type (fp32 for float/bf16, wrapping uint32 for int32).
+// Element traits. RAW is the caller dtype's bits, ACC the arithmetic type
+// (fp32 for float/bf16, wrapping uint32 for int32).
 
 struct F32 {
   using acc = float;
-  static constexpr int DW = 4;  // payload dwords per unit of raw elements
   static constexpr int kBytes = 4;
 };
 struct I32 {
   using acc = uint32_t;
-  static constexpr int DW = 4;
   static constexpr int kBytes = 4;
 };
 struct BF16 {
   using acc = float;
-  static constexpr int DW = 2;
   static constexpr int kBytes = 2;
 };
 
 __device__ __forceinline__ float acc_add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ uint32_t acc_add(uint32_t a, uint32_t b) { return a + b; }
-
-// raw dwords <-> 4 accumulators
-__device__ __forceinline__ void raw_to_acc(F32, const uint32_t (&d)[4], float (&a)[4]) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) a[k] = __uint_as_float(d[k]);
-}
-__device__ __forceinline__ void raw_to_acc(I32, const uint32_t (&d)[4], uint32_t (&a)[4]) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) a[k] = d[k];
-}
-__device__ __forceinline__ void raw_to_acc(BF16, const uint32_t (&d)[2], float (&a)[4]) {
-  a[0] = __uint_as_float(d[0] << 16);
-  a[1] = __uint_as_float(d[0] & 0xFFFF0000u);
-  a[2] = __uint_as_float(d[1] << 16);
-  a[3] = __uint_as_float(d[1] & 0xFFFF0000u);
-}
 
 __device__ __forceinline__ uint32_t f32_to_bf16_rne(float f) {
   uint32_t u = __float_as_uint(f);
@@ -290,97 +348,154 @@ __device__ __forceinline__ uint32_t f32_to_bf16_rne(float f) {
   return u >> 16;
 }
 
-__device__ __forceinline__ void acc_to_raw(F32, const float (&a)[4], uint32_t (&d)[4]) {
+// raw dwords (UE elements) <-> UE accumulators
+template <int UE>
+__device__ __forceinline__ void raw_to_acc(F32, const uint32_t (&d)[UE], float (&a)[UE]) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) d[k] = __float_as_uint(a[k]);
+  for (int k = 0; k < UE; ++k) a[k] = __uint_as_float(d[k]);
 }
-__device__ __forceinline__ void acc_to_raw(I32, const uint32_t (&a)[4], uint32_t (&d)[4]) {
+template <int UE>
+__device__ __forceinline__ void raw_to_acc(I32, const uint32_t (&d)[UE], uint32_t (&a)[UE]) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) d[k] = a[k];
+  for (int k = 0; k < UE; ++k) a[k] = d[k];
 }
-__device__ __forceinline__ void acc_to_raw(BF16, const float (&a)[4], uint32_t (&d)[2]) {
-  d[0] = f32_to_bf16_rne(a[0]) | (f32_to_bf16_rne(a[1]) << 16);
-  d[1] = f32_to_bf16_rne(a[2]) | (f32_to_bf16_rne(a[3]) << 16);
+template <int UE>
+__device__ __forceinline__ void raw_to_acc(BF16, const uint32_t (&d)[UE / 2], float (&a)[UE]) {
+#pragma unroll
+  for (int k = 0; k < UE / 2; ++k) {
+    a[2 * k] = __uint_as_float(d[k] << 16);
+    a[2 * k + 1] = __uint_as_float(d[k] & 0xFFFF0000u);
+  }
+}
+template <int UE>
+__device__ __forceinline__ void acc_to_raw(F32, const float (&a)[UE], uint32_t (&d)[UE]) {
+#pragma unroll
+  for (int k = 0; k < UE; ++k) d[k] = __float_as_uint(a[k]);
+}
+template <int UE>
+__device__ __forceinline__ void acc_to_raw(I32, const uint32_t (&a)[UE], uint32_t (&d)[UE]) {
+#pragma unroll
+  for (int k = 0; k < UE; ++k) d[k] = a[k];
+}
+template <int UE>
+__device__ __forceinline__ void acc_to_raw(BF16, const float (&a)[UE], uint32_t (&d)[UE / 2]) {
+#pragma unroll
+  for (int k = 0; k < UE / 2; ++k) {
+    d[k] = f32_to_bf16_rne(a[2 * k]) | (f32_to_bf16_rne(a[2 * k + 1]) << 16);
+  }
 }
 
-// acc <-> 4 payload dwords (recursive-doubling partials always travel as 4 dwords)
-__device__ __forceinline__ void acc_bits(const float (&a)[4], uint32_t (&d)[4]) {
+// accumulators <-> payload dwords (recursive-doubling partials)
+template <int UE>
+__device__ __forceinline__ void acc_bits(const float (&a)[UE], uint32_t (&d)[UE]) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) d[k] = __float_as_uint(a[k]);
+  for (int k = 0; k < UE; ++k) d[k] = __float_as_uint(a[k]);
 }
-__device__ __forceinline__ void acc_bits(const uint32_t (&a)[4], uint32_t (&d)[4]) {
+template <int UE>
+__device__ __forceinline__ void acc_bits(const uint32_t (&a)[UE], uint32_t (&d)[UE]) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) d[k] = a[k];
+  for (int k = 0; k < UE; ++k) d[k] = a[k];
 }
-__device__ __forceinline__ void bits_acc(const uint32_t (&d)[4], float (&a)[4]) {
+template <int UE>
+__device__ __forceinline__ void bits_acc(const uint32_t (&d)[UE], float (&a)[UE]) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) a[k] = __uint_as_float(d[k]);
+  for (int k = 0; k < UE; ++k) a[k] = __uint_as_float(d[k]);
 }
-__device__ __forceinline__ void bits_acc(const uint32_t (&d)[4], uint32_t (&a)[4]) {
+template <int UE>
+__device__ __forceinline__ void bits_acc(const uint32_t (&d)[UE], uint32_t (&a)[UE]) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) a[k] = d[k];
+  for (int k = 0; k < UE; ++k) a[k] = d[k];
 }
 
-// Load 4 raw elements starting at element index e of `p`, `valid` of them real
-// (the rest are the reference's zero padding, nvrar.hpp:99-104).
-template <class E>
+// Load UE raw elements starting at element index e of `p`, `valid` of them real
+// (the rest are the reference's zero padding, nvrar.hpp:99-104). RDW dwords.
+template <class E, int UE>
 __device__ __forceinline__ void load_raw(const void* p, uint64_t e, int valid,
-                                         uint32_t (&d)[E::DW]) {
+                                         uint32_t (&d)[UE * E::kBytes / 4]) {
+  constexpr int RDW = UE * E::kBytes / 4;
   if constexpr (E::kBytes == 4) {
     const uint32_t* q = static_cast<const uint32_t*>(p) + e;
-    if (valid == 4 && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(q));
-      d[0] = v.x;
-      d[1] = v.y;
-      d[2] = v.z;
-      d[3] = v.w;
+    if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+#pragma unroll
+      for (int h = 0; h < RDW / 4; ++h) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(q) + h);
+        d[4 * h] = v.x;
+        d[4 * h + 1] = v.y;
+        d[4 * h + 2] = v.z;
+        d[4 * h + 3] = v.w;
+      }
     } else {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) d[k] = k < valid ? __ldg(q + k) : 0u;
+      for (int k = 0; k < UE; ++k) d[k] = k < valid ? __ldg(q + k) : 0u;
     }
   } else {
     const uint16_t* q = static_cast<const uint16_t*>(p) + e;
-    if (valid == 4 && (reinterpret_cast<uintptr_t>(q) & 7u) == 0) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(q));
-      d[0] = v.x;
-      d[1] = v.y;
+    if constexpr (RDW == 4) {
+      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(q));
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+        return;
+      }
     } else {
-      uint32_t h[4];
+      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 7u) == 0) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(q));
+        d[0] = v.x;
+        d[1] = v.y;
+        return;
+      }
+    }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) h[k] = k < valid ? static_cast<uint32_t>(__ldg(q + k)) : 0u;
-      d[0] = h[0] | (h[1] << 16);
-      d[1] = h[2] | (h[3] << 16);
+    for (int k = 0; k < RDW; ++k) {
+      const uint32_t lo = 2 * k < valid ? static_cast<uint32_t>(__ldg(q + 2 * k)) : 0u;
+      const uint32_t hi = 2 * k + 1 < valid ? static_cast<uint32_t>(__ldg(q + 2 * k + 1)) : 0u;
+      d[k] = lo | (hi << 16);
     }
   }
 }
 
-template <class E>
+template <class E, int UE>
 __device__ __forceinline__ void store_raw(void* p, uint64_t e, int valid,
-                                          const uint32_t (&d)[E::DW]) {
+                                          const uint32_t (&d)[UE * E::kBytes / 4]) {
+  constexpr int RDW = UE * E::kBytes / 4;
   if constexpr (E::kBytes == 4) {
     uint32_t* q = static_cast<uint32_t*>(p) + e;
-    if (valid == 4 && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
-      *reinterpret_cast<uint4*>(q) = make_uint4(d[0], d[1], d[2], d[3]);
+    if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+#pragma unroll
+      for (int h = 0; h < RDW / 4; ++h) {
+        reinterpret_cast<uint4*>(q)[h] = make_uint4(d[4 * h], d[4 * h + 1], d[4 * h + 2], d[4 * h + 3]);
+      }
     } else {
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < UE; ++k)
         if (k < valid) q[k] = d[k];
     }
   } else {
     uint16_t* q = static_cast<uint16_t*>(p) + e;
-    if (valid == 4 && (reinterpret_cast<uintptr_t>(q) & 7u) == 0) {
-      *reinterpret_cast<uint2*>(q) = make_uint2(d[0], d[1]);
+    if constexpr (RDW == 4) {
+      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+        *reinterpret_cast<uint4*>(q) = make_uint4(d[0], d[1], d[2], d[3]);
+        return;
+      }
     } else {
-      const uint32_t h[4] = {d[0] & 0xFFFFu, d[0] >> 16, d[1] & 0xFFFFu, d[1] >> 16};
+      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 7u) == 0) {
+        *reinterpret_cast<uint2*>(q) = make_uint2(d[0], d[1]);
+        return;
+      }
+    }
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (k < valid) q[k] = static_cast<uint16_t>(h[k]);
+    for (int k = 0; k < RDW; ++k) {
+      if (2 * k < valid) q[2 * k] = static_cast<uint16_t>(d[k] & 0xFFFFu);
+      if (2 * k + 1 < valid) q[2 * k + 1] = static_cast<uint16_t>(d[k] >> 16);
     }
   }
 }
 
+template <int UE>
 __device__ __forceinline__ int clamp_valid(int64_t v) {
-  return v < 0 ? 0 : (v > 4 ? 4 : static_cast<int>(v));
+  return v < 0 ? 0 : (v > UE ? UE : static_cast<int>(v));
 }
 
 // Symmetric-region slot addressing.

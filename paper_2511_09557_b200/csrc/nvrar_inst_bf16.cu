@@ -2,5 +2,7 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_bf16(bool flat, int nodes, bool emu) { return kernel_for<BF16>(flat, nodes, emu); }
+KernelFn kernel_bf16(bool flat, int nodes, bool emu, bool lamport) {
+  return lamport ? kernel_for<BF16, true>(flat, nodes, emu) : kernel_for<BF16, false>(flat, nodes, emu);
+}
 }  // namespace nvrar

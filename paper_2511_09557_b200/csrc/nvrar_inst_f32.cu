@@ -2,5 +2,7 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_f32(bool flat, int nodes, bool emu) { return kernel_for<F32>(flat, nodes, emu); }
+KernelFn kernel_f32(bool flat, int nodes, bool emu, bool lamport) {
+  return lamport ? kernel_for<F32, true>(flat, nodes, emu) : kernel_for<F32, false>(flat, nodes, emu);
+}
 }  // namespace nvrar

@@ -2,5 +2,8 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_i32(bool flat, int nodes, bool emu) { return kernel_for<I32>(flat, nodes, emu); }
+KernelFn kernel_i32(bool flat, int nodes, bool emu, bool lamport) {
+  (void)lamport;  // int32 has no spare bit pattern: always LL
+  return kernel_for<I32, false>(flat, nodes, emu);
+}
 }  // namespace nvrar

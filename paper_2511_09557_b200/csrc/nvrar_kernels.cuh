@@ -13,8 +13,8 @@
 //
 // hier_kernel — the paper's three phases (nvrar.hpp:84-129):
 //   1. intra-group reduce-scatter: every rank pushes chunk c of its input to
-//      group member c over NVLink (LL words); member c folds its chunk in the
-//      pinned order with its own copy last;
+//      group member c over NVLink; member c folds its chunk in the pinned
+//      order with its own copy last;
 //   2. inter-group recursive doubling on the shard (nvrar.hpp:197-220): per
 //      unit, the running fp32/int32 partial goes to the XOR peer's per-step
 //      receive slot, the partner's arrives in ours, v = partner + own, and the
@@ -32,18 +32,31 @@
 //   two-shot = flat reduce-scatter (rank p owns elements [p*SP, (p+1)*SP)) +
 //   flat all-gather; one-shot = every rank receives every input.
 //
-// Reuse safety without any barrier: LL flags carry the call's sequence
-// number, and every slot set is double-buffered by seq parity
-// (nvrar.hpp:107-109,124-126). A rank can only write parity p again in call
-// k+2 after finishing call k+1, which needed data the reader sent only after
-// it had finished call k — so a slot is never overwritten before it is read.
+// Reuse safety without any barrier: every slot set is double-buffered by call
+// parity (nvrar.hpp:107-109,124-126) and re-emptied by its reader. A rank can
+// only write parity p again in call k+2 after finishing call k+1, which needed
+// data the reader sent only after it had finished call k (reads and re-empty
+// stores included) — so a slot is never overwritten before it is read.
 #pragma once
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "nvrar_device.cuh"
 
 namespace nvrar {
+
+// Protocol configuration per dtype: LL (fused words, 4 elements per unit) or
+// Lamport (raw payload, 16 bytes of elements per unit). RD partials are fp32 /
+// int32 accumulators and travel with the matching 4-byte protocol.
+template <class E, bool LAMPORT>
+struct Cfg {
+  using Raw = std::conditional_t<LAMPORT, Lamport<E::kBytes>, LL>;
+  using Part = std::conditional_t<LAMPORT, Lamport<4>, LL>;
+  static constexpr int UE = LAMPORT ? 16 / E::kBytes : 4;  // elements per unit
+  static constexpr int RDW = UE * E::kBytes / 4;           // raw dwords per unit
+};
 
 template <bool EMU>
 __device__ __forceinline__ const RankDesc& rank_desc(const LaunchParams& lp) {
@@ -116,21 +129,26 @@ struct Log2<1> {
 };
 
 // Real elements of unit u of the chunk starting at cbase with S elements: the
-// chunk boundary (not only n) bounds it, since S need not be a multiple of 4.
+// chunk boundary (not only n) bounds it, since S need not be a multiple of UE.
+template <int UE>
 __device__ __forceinline__ int chunk_valid(uint64_t S, uint64_t u, uint64_t n, uint64_t cbase) {
-  const int64_t in_chunk = static_cast<int64_t>(S) - static_cast<int64_t>(kUnit * u);
-  const int64_t in_vec = static_cast<int64_t>(n) - static_cast<int64_t>(cbase + kUnit * u);
-  return clamp_valid(in_chunk < in_vec ? in_chunk : in_vec);
+  const int64_t in_chunk = static_cast<int64_t>(S) - static_cast<int64_t>(UE * u);
+  const int64_t in_vec = static_cast<int64_t>(n) - static_cast<int64_t>(cbase + UE * u);
+  return clamp_valid<UE>(in_chunk < in_vec ? in_chunk : in_vec);
 }
 
 constexpr int kHierMaxG = 8;
 constexpr int kHierUpt = 2;  // units per thread carried through the RD steps together
 
 // ---------------------------------------------------------------------------
-template <class E, int N, bool EMU>
+template <class E, bool LAMPORT, int N, bool EMU>
 __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
-  constexpr int DW = E::DW;
+  using C = Cfg<E, LAMPORT>;
+  using Raw = typename C::Raw;
+  using Part = typename C::Part;
+  constexpr int UE = C::UE;
+  constexpr int RDW = C::RDW;
   constexpr int kSteps = Log2<N>::value;
   const RankDesc& d = rank_desc<EMU>(lp);
   Ctl c;
@@ -140,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   const uint64_t n = lp.count;
   const int G = d.gpus, me = d.rank, node = d.node, local = d.local;
   const uint64_t S = (n + G - 1) / G;
-  const uint64_t U = (S + kUnit - 1) / kUnit;
+  const uint64_t U = (S + UE - 1) / UE;
   const uint64_t ub = U * blockIdx.x / gridDim.x;
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
@@ -158,11 +176,11 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       uint4* slot = slot_a(d, node * G + cc, parity, local);
       const uint64_t cbase = static_cast<uint64_t>(cc) * S;
       for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-        const int valid = chunk_valid(S, u, n, cbase);
+        const int valid = chunk_valid<UE>(S, u, n, cbase);
         if (valid == 0) continue;  // pure padding: skipped identically by the reader
-        uint32_t raw[DW];
-        load_raw<E>(send, cbase + kUnit * u, valid, raw);
-        ll_store<DW>(slot, u, raw, c.seq);
+        uint32_t raw[RDW];
+        load_raw<E, UE>(send, cbase + UE * u, valid, raw);
+        Raw::template put<RDW>(slot, u, raw, c.seq);
       }
     }
   }
@@ -180,53 +198,56 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   // Phases 1b+2+3a: fold own chunk, recursive doubling, cast + all-gather push.
   const uint64_t mybase = static_cast<uint64_t>(local) * S;
   for (uint64_t u0 = ub + threadIdx.x; u0 < ue; u0 += static_cast<uint64_t>(blockDim.x) * kHierUpt) {
-    A f[kHierUpt][4];
+    A f[kHierUpt][UE];
     int valid[kHierUpt];
     uint64_t uu[kHierUpt];
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
       uu[k] = u0 + static_cast<uint64_t>(k) * blockDim.x;
-      valid[k] = uu[k] < ue ? chunk_valid(S, uu[k], n, mybase) : 0;
+      valid[k] = uu[k] < ue ? chunk_valid<UE>(S, uu[k], n, mybase) : 0;
     }
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
       if (valid[k] == 0) continue;
-      uint32_t own[DW];
-      load_raw<E>(send, mybase + kUnit * uu[k], valid[k], own);
+      uint32_t own[RDW];
+      load_raw<E, UE>(send, mybase + UE * uu[k], valid[k], own);
       if (G == 1) {
-        raw_to_acc(E{}, own, f[k]);
+        raw_to_acc<UE>(E{}, own, f[k]);
         continue;
       }
-      uint32_t r[kHierMaxG - 1][DW];
+      uint32_t r[kHierMaxG - 1][RDW];
       bool ok[kHierMaxG - 1];
       uint32_t bad = 0;
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
-        if (j < G) ok[j - 1] = ll_try<DW>(slot_a(d, me, parity, (local + j) % G), uu[k], c.seq,
-                                          r[j - 1], bad);
+        if (j < G) {
+          ok[j - 1] = Raw::template try_get<RDW>(slot_a(d, me, parity, (local + j) % G), uu[k],
+                                                 c.seq, r[j - 1], bad);
+          if (ok[j - 1]) Raw::template clear<RDW>(slot_a(d, me, parity, (local + j) % G), uu[k]);
+        }
       }
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G && !ok[j - 1]) {
           const int s = (local + j) % G;
-          ll_wait<DW>(c, slot_a(d, me, parity, s), uu[k], r[j - 1], node * G + s);
+          recv_unit<Raw, RDW>(c, slot_a(d, me, parity, s), uu[k], r[j - 1], node * G + s);
         }
       }
       // c owns in[c] + (in[c-1] + (... + (in[c+2] + in[c+1])))  (ring_schedule.hpp:12-15)
-      raw_to_acc(E{}, r[0], f[k]);
+      raw_to_acc<UE>(E{}, r[0], f[k]);
 #pragma unroll
       for (int j = 2; j < kHierMaxG; ++j) {
         if (j < G) {
-          A a[4];
-          raw_to_acc(E{}, r[j - 1], a);
+          A a[UE];
+          raw_to_acc<UE>(E{}, r[j - 1], a);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) f[k][q] = acc_add(f[k][q], a[q]);
+          for (int q = 0; q < UE; ++q) f[k][q] = acc_add(f[k][q], a[q]);
         }
       }
-      A a[4];
-      raw_to_acc(E{}, own, a);
+      A a[UE];
+      raw_to_acc<UE>(E{}, own, a);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) f[k][q] = acc_add(f[k][q], a[q]);
+      for (int q = 0; q < UE; ++q) f[k][q] = acc_add(f[k][q], a[q]);
     }
 
     // Recursive doubling (rd_block, nvrar.hpp:197-220): v = partner + own.
@@ -237,20 +258,20 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
       for (int k = 0; k < kHierUpt; ++k) {
         if (valid[k] == 0) continue;
-        uint32_t b[4];
-        acc_bits(f[k], b);
-        ll_store<4>(dst, uu[k], b, c.seq);
+        uint32_t b[UE];
+        acc_bits<UE>(f[k], b);
+        Part::template put<UE>(dst, uu[k], b, c.seq);
       }
-      const uint4* src = slot_c(d, me, parity, l);
+      uint4* src = slot_c(d, me, parity, l);
 #pragma unroll
       for (int k = 0; k < kHierUpt; ++k) {
         if (valid[k] == 0) continue;
-        uint32_t b[4];
-        ll_wait<4>(c, src, uu[k], b, partner);
-        A p[4];
-        bits_acc(b, p);
+        uint32_t b[UE];
+        recv_unit<Part, UE>(c, src, uu[k], b, partner);
+        A p[UE];
+        bits_acc<UE>(b, p);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) f[k][q] = acc_add(p[q], f[k][q]);
+        for (int q = 0; q < UE; ++q) f[k][q] = acc_add(p[q], f[k][q]);
       }
     }
 
@@ -258,11 +279,12 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
       if (valid[k] == 0) continue;
-      uint32_t o[DW];
-      acc_to_raw(E{}, f[k], o);
-      store_raw<E>(recv, mybase + kUnit * uu[k], valid[k], o);
+      uint32_t o[RDW];
+      acc_to_raw<UE>(E{}, f[k], o);
+      store_raw<E, UE>(recv, mybase + UE * uu[k], valid[k], o);
       for (int j = 1; j < G; ++j) {
-        ll_store<DW>(slot_b(d, node * G + (local + j) % G, parity, local), uu[k], o, c.seq);
+        Raw::template put<RDW>(slot_b(d, node * G + (local + j) % G, parity, local), uu[k], o,
+                               c.seq);
       }
     }
   }
@@ -271,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   // Phase 3b: all-gather receive.
   if (G > 1) {
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-      uint32_t r[kHierMaxG - 1][DW];
+      uint32_t r[kHierMaxG - 1][RDW];
       bool ok[kHierMaxG - 1];
       int valid[kHierMaxG - 1];
       uint32_t bad = 0;
@@ -279,18 +301,21 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G) {
           const int s = (local + j) % G;
-          valid[j - 1] = chunk_valid(S, u, n, static_cast<uint64_t>(s) * S);
-          ok[j - 1] = valid[j - 1] == 0 ||
-                      ll_try<DW>(slot_b(d, me, parity, s), u, c.seq, r[j - 1], bad);
+          valid[j - 1] = chunk_valid<UE>(S, u, n, static_cast<uint64_t>(s) * S);
+          ok[j - 1] = valid[j - 1] == 0;
+          if (!ok[j - 1]) {
+            ok[j - 1] = Raw::template try_get<RDW>(slot_b(d, me, parity, s), u, c.seq, r[j - 1], bad);
+            if (ok[j - 1]) Raw::template clear<RDW>(slot_b(d, me, parity, s), u);
+          }
         }
       }
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G) {
           const int s = (local + j) % G;
-          if (!ok[j - 1]) ll_wait<DW>(c, slot_b(d, me, parity, s), u, r[j - 1], node * G + s);
+          if (!ok[j - 1]) recv_unit<Raw, RDW>(c, slot_b(d, me, parity, s), u, r[j - 1], node * G + s);
           if (valid[j - 1] > 0) {
-            store_raw<E>(recv, static_cast<uint64_t>(s) * S + kUnit * u, valid[j - 1], r[j - 1]);
+            store_raw<E, UE>(recv, static_cast<uint64_t>(s) * S + UE * u, valid[j - 1], r[j - 1]);
           }
         }
       }
@@ -304,28 +329,32 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 // Flat schedules. MAXG bounds gpus_per_node so the N x MAXG source units live
 // in statically indexed registers.
 
-template <class E, int N, int MAXG>
-__device__ __forceinline__ typename E::acc pick(const uint32_t (&r)[N][MAXG][E::DW], int nn,
+template <class E, int UE, int RDW, int N, int MAXG>
+__device__ __forceinline__ typename E::acc pick(const uint32_t (&r)[N][MAXG][RDW], int nn,
                                                 int idx, int k) {
   using A = typename E::acc;
   A v{};
 #pragma unroll
   for (int t = 0; t < MAXG; ++t) {
     if (t == idx) {
-      A a[4];
-      raw_to_acc(E{}, r[nn][t], a);
+      A a[UE];
+      raw_to_acc<UE>(E{}, r[nn][t], a);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < UE; ++q)
         if (q == k) v = a[q];
     }
   }
   return v;
 }
 
-template <class E, int N, int MAXG, bool EMU>
+template <class E, bool LAMPORT, int N, int MAXG, bool EMU>
 __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
-  constexpr int DW = E::DW;
+  using C = Cfg<E, LAMPORT>;
+  using Raw = typename C::Raw;
+  constexpr int UE = C::UE;
+  constexpr int RDW = C::RDW;
+  constexpr int kLevels = Log2<N>::value + 1;
   const RankDesc& d = rank_desc<EMU>(lp);
   Ctl c;
   if (!begin_call(d, c)) return;
@@ -335,8 +364,10 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const int G = d.gpus, P = d.world, me = d.rank;
   const bool oneshot = lp.oneshot != 0;
   const uint64_t SG = (n + G - 1) / G;
-  const uint64_t SP = oneshot ? ((n + 3) & ~3ull) : ((((n + P - 1) / P) + 3) & ~3ull);
-  const uint64_t U = SP / kUnit;
+  constexpr uint64_t kAlign = UE;
+  const uint64_t SP = oneshot ? ((n + kAlign - 1) / kAlign) * kAlign
+                              : ((((n + P - 1) / P) + kAlign - 1) / kAlign) * kAlign;
+  const uint64_t U = SP / UE;
   const uint64_t ub = U * blockIdx.x / gridDim.x;
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
@@ -354,12 +385,12 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     const uint64_t qbase = oneshot ? 0 : static_cast<uint64_t>(q) * SP;
     uint4* slot = slot_a(d, q, parity, me);
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-      const uint64_t e = qbase + kUnit * u;
-      const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e));
+      const uint64_t e = qbase + UE * u;
+      const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e));
       if (valid == 0) continue;
-      uint32_t raw[DW];
-      load_raw<E>(send, e, valid, raw);
-      ll_store<DW>(slot, u, raw, c.seq);
+      uint32_t raw[RDW];
+      load_raw<E, UE>(send, e, valid, raw);
+      Raw::template put<RDW>(slot, u, raw, c.seq);
     }
   }
   stamp(d, 2);
@@ -372,15 +403,15 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 
   const uint64_t mybase = oneshot ? 0 : static_cast<uint64_t>(me) * SP;
   for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-    const uint64_t e0 = mybase + kUnit * u;
-    const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+    const uint64_t e0 = mybase + UE * u;
+    const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
     if (valid == 0) continue;
     const int c0 = static_cast<int>(e0 / SG);
     const int c3 = static_cast<int>((e0 + valid - 1) / SG);
 
     // Every source's unit, in fold order relative to c0: r[nn][j] is the copy
     // of local rank (c0+1+j) % G of node nn.
-    uint32_t r[N][MAXG][DW];
+    uint32_t r[N][MAXG][RDW];
     bool ok[N][MAXG];
     uint32_t bad = 0;
 #pragma unroll
@@ -391,9 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         if (j < G) {
           const int s = nn * G + (c0 + 1 + j) % G;
           if (s == me) {
-            load_raw<E>(send, e0, valid, r[nn][j]);
+            load_raw<E, UE>(send, e0, valid, r[nn][j]);
           } else {
-            ok[nn][j] = ll_try<DW>(slot_a(d, me, parity, s), u, c.seq, r[nn][j], bad);
+            ok[nn][j] = Raw::template try_get<RDW>(slot_a(d, me, parity, s), u, c.seq, r[nn][j], bad);
+            if (ok[nn][j]) Raw::template clear<RDW>(slot_a(d, me, parity, s), u);
           }
         }
       }
@@ -404,57 +436,67 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       for (int j = 0; j < MAXG; ++j) {
         if (j < G && !ok[nn][j]) {
           const int s = nn * G + (c0 + 1 + j) % G;
-          ll_wait<DW>(c, slot_a(d, me, parity, s), u, r[nn][j], s);
+          recv_unit<Raw, RDW>(c, slot_a(d, me, parity, s), u, r[nn][j], s);
         }
       }
     }
 
-    A part[N][4];
-    if (c0 == c3) {
+    // Node partials, combined on the fly into the pairwise tree over nodes
+    // (node order == the XOR-step adds): stack[k] holds a finished subtree of
+    // 2^k nodes.
+    A stack[kLevels][UE];
 #pragma unroll
-      for (int nn = 0; nn < N; ++nn) {
-        raw_to_acc(E{}, r[nn][0], part[nn]);
+    for (int nn = 0; nn < N; ++nn) {
+      A v[UE];
+      if (c0 == c3) {
+        raw_to_acc<UE>(E{}, r[nn][0], v);
 #pragma unroll
         for (int j = 1; j < MAXG; ++j) {
           if (j < G) {
-            A a[4];
-            raw_to_acc(E{}, r[nn][j], a);
+            A a[UE];
+            raw_to_acc<UE>(E{}, r[nn][j], a);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) part[nn][q] = acc_add(part[nn][q], a[q]);
+            for (int q = 0; q < UE; ++q) v[q] = acc_add(v[q], a[q]);
           }
         }
-      }
-    } else {
-      // The unit straddles a shard boundary: per-element fold order.
+      } else {
+        // The unit straddles a shard boundary: per-element fold order.
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int cq = q < valid ? static_cast<int>((e0 + q) / SG) : c0;
-        const int rot = cq - c0;
-#pragma unroll
-        for (int nn = 0; nn < N; ++nn) {
-          A v = pick<E, N, MAXG>(r, nn, rot % G, q);
+        for (int q = 0; q < UE; ++q) {
+          const int cq = q < valid ? static_cast<int>((e0 + q) / SG) : c0;
+          const int rot = cq - c0;
+          A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % G, q);
 #pragma unroll
           for (int j = 1; j < MAXG; ++j) {
-            if (j < G) v = acc_add(v, pick<E, N, MAXG>(r, nn, (j + rot) % G, q));
+            if (j < G) x = acc_add(x, pick<E, UE, RDW, N, MAXG>(r, nn, (j + rot) % G, q));
           }
-          part[nn][q] = v;
+          v[q] = x;
+        }
+      }
+      int lvl = 0;
+#pragma unroll
+      for (int k = 0; k < kLevels - 1; ++k) {
+        if (((nn >> k) & 1) && lvl == k) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) v[q] = acc_add(stack[k][q], v[q]);
+          lvl = k + 1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kLevels; ++k) {
+        if (k == lvl) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) stack[k][q] = v[q];
         }
       }
     }
-    // Pairwise tree over nodes in node order == the XOR-step adds.
-#pragma unroll
-    for (int w = 1; w < N; w <<= 1) {
-#pragma unroll
-      for (int nn = 0; nn + w < N; nn += 2 * w) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) part[nn][q] = acc_add(part[nn][q], part[nn + w][q]);
-      }
-    }
-    uint32_t o[DW];
-    acc_to_raw(E{}, part[0], o);
-    store_raw<E>(recv, e0, valid, o);
+    uint32_t o[RDW];
+    acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
+    store_raw<E, UE>(recv, e0, valid, o);
     if (!oneshot) {
-      for (int j = 1; j < P; ++j) ll_store<DW>(slot_b(d, (me + j) % P, parity, me), u, o, c.seq);
+      for (int j = 1; j < P; ++j) {
+        Raw::template put<RDW>(slot_b(d, (me + j) % P, parity, me), u, o, c.seq);
+      }
     }
   }
   stamp(d, 4);
@@ -463,12 +505,12 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
       for (int j = 1; j < P; ++j) {
         const int q = (me + P - j) % P;
-        const uint64_t e0 = static_cast<uint64_t>(q) * SP + kUnit * u;
-        const int valid = clamp_valid(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+        const uint64_t e0 = static_cast<uint64_t>(q) * SP + UE * u;
+        const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
         if (valid == 0) continue;
-        uint32_t r[DW];
-        ll_wait<DW>(c, slot_b(d, me, parity, q), u, r, q);
-        store_raw<E>(recv, e0, valid, r);
+        uint32_t r[RDW];
+        recv_unit<Raw, RDW>(c, slot_b(d, me, parity, q), u, r, q);
+        store_raw<E, UE>(recv, e0, valid, r);
       }
     }
   }
@@ -478,36 +520,36 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 
 using KernelFn = void (*)(LaunchParams);
 
-template <class E, bool EMU>
+template <class E, bool LAMPORT, bool EMU>
 KernelFn hier_for(int nodes) {
   switch (nodes) {
-    case 1: return hier_kernel<E, 1, EMU>;
-    case 2: return hier_kernel<E, 2, EMU>;
-    case 4: return hier_kernel<E, 4, EMU>;
-    case 8: return hier_kernel<E, 8, EMU>;
+    case 1: return hier_kernel<E, LAMPORT, 1, EMU>;
+    case 2: return hier_kernel<E, LAMPORT, 2, EMU>;
+    case 4: return hier_kernel<E, LAMPORT, 4, EMU>;
+    case 8: return hier_kernel<E, LAMPORT, 8, EMU>;
     default: return nullptr;
   }
 }
 
-template <class E, bool EMU>
+template <class E, bool LAMPORT, bool EMU>
 KernelFn flat_for(int nodes) {
   switch (nodes) {
-    case 1: return flat_kernel<E, 1, 8, EMU>;
-    case 2: return flat_kernel<E, 2, 8, EMU>;
-    case 4: return flat_kernel<E, 4, 4, EMU>;
-    case 8: return flat_kernel<E, 8, 2, EMU>;
+    case 1: return flat_kernel<E, LAMPORT, 1, 8, EMU>;
+    case 2: return flat_kernel<E, LAMPORT, 2, 8, EMU>;
+    case 4: return flat_kernel<E, LAMPORT, 4, 4, EMU>;
+    case 8: return flat_kernel<E, LAMPORT, 8, 2, EMU>;
     default: return nullptr;
   }
 }
 
-template <class E>
+template <class E, bool LAMPORT>
 KernelFn kernel_for(bool flat, int nodes, bool emu) {
-  if (flat) return emu ? flat_for<E, true>(nodes) : flat_for<E, false>(nodes);
-  return emu ? hier_for<E, true>(nodes) : hier_for<E, false>(nodes);
+  if (flat) return emu ? flat_for<E, LAMPORT, true>(nodes) : flat_for<E, LAMPORT, false>(nodes);
+  return emu ? hier_for<E, LAMPORT, true>(nodes) : hier_for<E, LAMPORT, false>(nodes);
 }
 
-KernelFn kernel_f32(bool flat, int nodes, bool emu);
-KernelFn kernel_bf16(bool flat, int nodes, bool emu);
-KernelFn kernel_i32(bool flat, int nodes, bool emu);
+KernelFn kernel_f32(bool flat, int nodes, bool emu, bool lamport);
+KernelFn kernel_bf16(bool flat, int nodes, bool emu, bool lamport);
+KernelFn kernel_i32(bool flat, int nodes, bool emu, bool lamport);
 
 }  // namespace nvrar

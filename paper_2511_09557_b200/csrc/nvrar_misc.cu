@@ -39,11 +39,11 @@ __global__ void pingpong_kernel(const __grid_constant__ LaunchParams lp, int pee
   *out_ns = globaltimer() - t0;
 }
 
-KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu) {
+KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu, bool lamport) {
   switch (dtype) {
-    case 0: return kernel_i32(flat, nodes, emu);
-    case 1: return kernel_f32(flat, nodes, emu);
-    case 2: return kernel_bf16(flat, nodes, emu);
+    case 0: return kernel_i32(flat, nodes, emu, false);
+    case 1: return kernel_f32(flat, nodes, emu, lamport);
+    case 2: return kernel_bf16(flat, nodes, emu, lamport);
     default: return nullptr;
   }
 }

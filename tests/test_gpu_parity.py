@@ -71,8 +71,9 @@ def from_dev(t, dtype):
     return t.cpu().numpy()
 
 
-def run(g, x, dtype, algo="auto", cfg=None, active=None):
+def run(g, x, dtype, algo="auto", cfg=None, active=None, proto="auto"):
     g.set_algo(algo)
+    g.set_protocol(proto)
     ins = [to_dev(x[r], dtype) for r in range(x.shape[0])]
     outs = [torch.empty_like(t) for t in ins]
     g.run_all(ins, outs, cfg=cfg or NvrarConfig(), active=active)
@@ -94,14 +95,41 @@ HIERS = [(1, 1), (1, 2), (2, 1), (1, 4), (2, 2), (4, 1), (1, 8), (2, 4), (4, 2),
 
 @pytest.mark.parametrize("nodes,gpus", HIERS)
 @pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
-def test_parity_hierarchies(nodes, gpus, algo, dtype):
+@pytest.mark.parametrize("dtype,proto", [("f32", "lamport"), ("f32", "ll"), ("bf16", "lamport"),
+                                         ("bf16", "ll"), ("i32", "auto")])
+def test_parity_hierarchies(nodes, gpus, algo, dtype, proto):
     if algo != "hier" and not flat_ok(nodes, gpus):
         pytest.skip("flat schedules cover P <= 16 within MAXG")
     g = group(nodes, gpus)
     for n in (1, 7, 1031, 65539):
         x = inputs_for(dtype, nodes * gpus, n, 19 + n)
-        assert_parity(run(g, x, dtype, algo), x, nodes, gpus, dtype)
+        assert_parity(run(g, x, dtype, algo, proto=proto), x, nodes, gpus, dtype)
+    g.set_protocol("auto")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_lamport_sentinel_pattern_is_data_not_a_hang(algo, dtype):
+    """An all-ones input (the Lamport 'empty' pattern, a NaN) must travel as a NaN
+    and never stall the receiver; every other element stays bit-exact."""
+    g = group(2, 4)
+    x = inputs_for(dtype, 8, 4099, 3)
+    if dtype == "f32":
+        xv = x.view(np.uint32)
+        xv[3, 10] = 0xFFFFFFFF
+        xv[0, 4000] = 0xFFFFFFFF
+    else:
+        x[3, 10] = 0xFFFF
+        x[0, 4000] = 0xFFFF
+    out = run(g, x, dtype, algo, proto="lamport")
+    want = O.nvrar_order_sum(x, 2, 4, dtype)
+    f = (lambda a: a.view(np.float32)) if dtype == "f32" else O.f32_from_bf16_bits
+    for r in range(8):
+        got = f(out[r])
+        assert np.isnan(got[10]) and np.isnan(got[4000])
+        keep = np.ones(4099, bool)
+        keep[[10, 4000]] = False
+        assert np.array_equal(out[r][keep], want[keep])
 
 
 @pytest.mark.parametrize("algo", ALGOS)
