@@ -1,0 +1,42 @@
+"""Single-process driver for ncu captures: the N=1 bench workload (2x4 virtual
+ranks on cuda:0, one cooperative launch per all-reduce) run eagerly a few
+times, so `ncu -k regex:<kernel>` can pick one launch.
+
+    python -m paper_2511_09557_b200.profile_emu --algo twoshot --dtype f32 --bytes 1048576
+"""
+from __future__ import annotations
+
+import argparse
+
+import torch
+
+from .comm import ClusterTopology, LocalGroup
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--algo", default="auto")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--bytes", type=int, default=1 << 20)
+    ap.add_argument("--calls", type=int, default=6)
+    ap.add_argument("--nodes", type=int, default=2)
+    ap.add_argument("--gpus", type=int, default=4)
+    ap.add_argument("--proto", default="auto")
+    args = ap.parse_args()
+    dt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    n = args.bytes // (4 if args.dtype == "f32" else 2)
+    p = args.nodes * args.gpus
+    g = LocalGroup(ClusterTopology(args.nodes, args.gpus), max(args.bytes, 1 << 20), device=0)
+    g.set_algo(args.algo)
+    g.set_protocol(args.proto)
+    ins = [torch.randn(n, device="cuda").to(dt) for _ in range(p)]
+    outs = [torch.empty_like(t) for t in ins]
+    for _ in range(args.calls):
+        g.launch(ins, outs)
+    g.check()
+    print("plan", g.comms[0].plan(n, dt), "ok")
+    g.close()
+
+
+if __name__ == "__main__":
+    main()
