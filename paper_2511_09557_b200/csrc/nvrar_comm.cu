@@ -634,7 +634,7 @@ int nvrar_get_phase_times(nvrar_comm_t c, uint64_t* ts, int n) {
   CUDA_TRY(c, cudaDeviceSynchronize());
   RankState st;
   CUDA_TRY(c, cudaMemcpy(&st, c->state, sizeof(st), cudaMemcpyDeviceToHost));
-  for (int i = 0; i < n && i < kPhases; ++i) ts[i] = st.ts[i];
+  for (int i = 0; i < n && i < kSeqSlots * kPhases; ++i) ts[i] = (&st.ts[0][0])[i];
   return NVRAR_SUCCESS;
 }
 

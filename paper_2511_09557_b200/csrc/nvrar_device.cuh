@@ -76,7 +76,7 @@ constexpr int kPhases = 8;
 struct RankState {
   uint32_t seq[kSeqSlots];
   ErrRec err;
-  uint64_t ts[kPhases];  // phase timestamps of CTA 0, thread 0 (profiling)
+  uint64_t ts[kSeqSlots][kPhases];  // per-CTA phase timestamps, thread 0 (profiling)
 };
 
 struct RankDesc {
@@ -527,7 +527,7 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 
 __device__ __forceinline__ void stamp(const RankDesc& d, int k) {
-  if (d.profile && blockIdx.x == 0 && threadIdx.x == 0) d.state->ts[k] = globaltimer();
+  if (d.profile && threadIdx.x == 0) d.state->ts[blockIdx.x][k] = globaltimer();
 }
 
 }  // namespace nvrar

@@ -67,12 +67,19 @@ __device__ __forceinline__ const RankDesc& rank_desc(const LaunchParams& lp) {
   }
 }
 
-// Prologue. Returns false when the communicator carries a sticky fault.
-__device__ __forceinline__ bool begin_call(const RankDesc& d, Ctl& c) {
-  __shared__ uint32_t s_seq, s_err;
+// Prologue, part 1: wait for the previous kernel on the stream (the previous
+// call, or the producer of our input) and let the next launch start early.
+__device__ __forceinline__ void begin_wait(const RankDesc& d) {
   stamp(d, 0);
-  pdl_wait();  // the previous call (and the producer of our input) is complete
+  pdl_wait();
   pdl_launch_dependents();
+  stamp(d, 7);
+}
+
+// Prologue, part 2 (after the caller has issued its first input loads, which
+// do not depend on the call number). Returns false on a sticky fault.
+__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
+  __shared__ uint32_t s_seq, s_err;
   if (threadIdx.x == 0) {
     s_err = ld_volatile32(&d.state->err.code);
     s_seq = ld_volatile32(&d.state->seq[blockIdx.x]);
@@ -151,10 +158,6 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   constexpr int RDW = C::RDW;
   constexpr int kSteps = Log2<N>::value;
   const RankDesc& d = rank_desc<EMU>(lp);
-  Ctl c;
-  if (!begin_call(d, c)) return;  // sticky fault: comm is dead
-  const uint32_t parity = c.seq & 1u;
-
   const uint64_t n = lp.count;
   const int G = d.gpus, me = d.rank, node = d.node, local = d.local;
   const uint64_t S = (n + G - 1) / G;
@@ -163,6 +166,25 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
   void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
+  const uint64_t u_first = ub + threadIdx.x;
+
+  begin_wait(d);
+  // Prefetch this thread's first unit of every chunk before the call number is
+  // read (the loads do not depend on it): pre[j] = chunk (local + j) % G.
+  uint32_t pre[kHierMaxG][RDW];
+  int pv[kHierMaxG];
+#pragma unroll
+  for (int j = 0; j < kHierMaxG; ++j) {
+    pv[j] = 0;
+    if (j < G && u_first < ue) {
+      const uint64_t cbase = static_cast<uint64_t>((local + j) % G) * S;
+      pv[j] = chunk_valid<UE>(S, u_first, n, cbase);
+      if (pv[j] > 0) load_raw<E, UE>(send, cbase + UE * u_first, pv[j], pre[j]);
+    }
+  }
+  Ctl c;
+  if (!begin_seq(d, c)) return;  // sticky fault: comm is dead
+  const uint32_t parity = c.seq & 1u;
 
   // Peer-only sync, publish half (nvrar.hpp:163-171).
   if (kSteps > 0 && blockIdx.x == 0 && threadIdx.x < kSteps) {
@@ -171,11 +193,18 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 
   // Phase 1a: reduce-scatter pushes (ring_reduce_scatter_phase, ring_schedule.hpp:33-58).
   if (G > 1) {
+#pragma unroll
+    for (int j = 1; j < kHierMaxG; ++j) {
+      if (j < G && pv[j] > 0) {
+        Raw::template put<RDW>(slot_a(d, node * G + (local + j) % G, parity, local), u_first,
+                               pre[j], c.seq);
+      }
+    }
     for (int j = 1; j < G; ++j) {
       const int cc = (local + j) % G;
       uint4* slot = slot_a(d, node * G + cc, parity, local);
       const uint64_t cbase = static_cast<uint64_t>(cc) * S;
-      for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+      for (uint64_t u = u_first + blockDim.x; u < ue; u += blockDim.x) {
         const int valid = chunk_valid<UE>(S, u, n, cbase);
         if (valid == 0) continue;  // pure padding: skipped identically by the reader
         uint32_t raw[RDW];
@@ -210,7 +239,12 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     for (int k = 0; k < kHierUpt; ++k) {
       if (valid[k] == 0) continue;
       uint32_t own[RDW];
-      load_raw<E, UE>(send, mybase + UE * uu[k], valid[k], own);
+      if (k == 0 && u0 == u_first) {
+#pragma unroll
+        for (int q = 0; q < RDW; ++q) own[q] = pre[0][q];
+      } else {
+        load_raw<E, UE>(send, mybase + UE * uu[k], valid[k], own);
+      }
       if (G == 1) {
         raw_to_acc<UE>(E{}, own, f[k]);
         continue;
@@ -356,10 +390,6 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   constexpr int RDW = C::RDW;
   constexpr int kLevels = Log2<N>::value + 1;
   const RankDesc& d = rank_desc<EMU>(lp);
-  Ctl c;
-  if (!begin_call(d, c)) return;
-  const uint32_t parity = c.seq & 1u;
-
   const uint64_t n = lp.count;
   const int G = d.gpus, P = d.world, me = d.rank;
   const bool oneshot = lp.oneshot != 0;
@@ -372,6 +402,27 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
   void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
+  const uint64_t u_first = ub + threadIdx.x;
+
+  begin_wait(d);
+  // Prefetch this thread's first unit of every sub-shard (pre[j]: owner
+  // (me + j) % P; j = 0 is our own) before the call number is read. One-shot
+  // sends the same unit to everyone, so it loads once.
+  constexpr int kPre = 8;
+  uint32_t pre[kPre][RDW];
+  int pv[kPre];
+#pragma unroll
+  for (int j = 0; j < kPre; ++j) {
+    pv[j] = 0;
+    if (j < P && u_first < ue && (!oneshot || j == 0)) {
+      const uint64_t e = (oneshot ? 0 : static_cast<uint64_t>((me + j) % P) * SP) + UE * u_first;
+      pv[j] = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e));
+      if (pv[j] > 0) load_raw<E, UE>(send, e, pv[j], pre[j]);
+    }
+  }
+  Ctl c;
+  if (!begin_seq(d, c)) return;
+  const uint32_t parity = c.seq & 1u;
 
   if (blockIdx.x == 0) {
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
@@ -380,11 +431,20 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   }
 
   // Reduce-scatter pushes: the owner q of each sub-shard receives our copy.
+#pragma unroll
+  for (int j = 1; j < kPre; ++j) {
+    if (j < P) {
+      const int src = oneshot ? 0 : j;
+      if (pv[src] > 0) {
+        Raw::template put<RDW>(slot_a(d, (me + j) % P, parity, me), u_first, pre[src], c.seq);
+      }
+    }
+  }
   for (int j = 1; j < P; ++j) {
     const int q = (me + j) % P;
     const uint64_t qbase = oneshot ? 0 : static_cast<uint64_t>(q) * SP;
     uint4* slot = slot_a(d, q, parity, me);
-    for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+    for (uint64_t u = (j < kPre ? u_first + blockDim.x : u_first); u < ue; u += blockDim.x) {
       const uint64_t e = qbase + UE * u;
       const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e));
       if (valid == 0) continue;
@@ -421,7 +481,10 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         ok[nn][j] = true;
         if (j < G) {
           const int s = nn * G + (c0 + 1 + j) % G;
-          if (s == me) {
+          if (s == me && u == u_first) {
+#pragma unroll
+            for (int q = 0; q < RDW; ++q) r[nn][j][q] = pre[0][q];
+          } else if (s == me) {
             load_raw<E, UE>(send, e0, valid, r[nn][j]);
           } else {
             ok[nn][j] = Raw::template try_get<RDW>(slot_a(d, me, parity, s), u, c.seq, r[nn][j], bad);

@@ -114,10 +114,24 @@ def main():
         g = graph_of(lambda i: comm.allreduce(*bufs[i % nbuf]), 20, stream)
         g.replay()
         torch.cuda.synchronize()
-        tsb = (ctypes.c_uint64 * 8)()
-        comm._lib.nvrar_get_phase_times(comm._h, tsb, 8)
-        rel = [(tsb[i] - tsb[0]) / 1e3 for i in range(7)]
-        phases[str(size)] = [round(v, 3) for v in D.max_over_ranks(rel)]
+        tsb = (ctypes.c_uint64 * (512 * 8))()
+        comm._lib.nvrar_get_phase_times(comm._h, tsb, 512 * 8)
+        nb = best[str(size)][1]
+        cta = [[tsb[b * 8 + i] for i in range(8)] for b in range(nb)]  # [7] = released
+        t0 = min(c[7] for c in cta)  # earliest release of the last call
+        rel = [(cta[0][i] - cta[0][0]) / 1e3 for i in range(8)]
+        summary = [
+            (max(c[7] for c in cta) - t0) / 1e3,                        # release spread
+            statistics.median((c[6] - c[7]) / 1e3 for c in cta),         # median CTA work
+            (max(c[6] for c in cta) - t0) / 1e3,                        # last exit
+            statistics.median((c[7] - c[0]) / 1e3 for c in cta),         # median entry->release
+            statistics.median((c[2] - c[7]) / 1e3 for c in cta),         # release->pushed
+            statistics.median((c[3] - c[2]) / 1e3 for c in cta),         # pushed->synced
+            statistics.median((c[4] - c[3]) / 1e3 for c in cta),         # synced->reduced
+            statistics.median((c[5] - c[4]) / 1e3 for c in cta),         # reduced->ag recv
+        ]
+        phases[str(size)] = {"cta0": [round(v, 3) for v in D.max_over_ranks(rel)],
+                             "summary": [round(v, 3) for v in D.max_over_ranks(summary)]}
         comm._lib.nvrar_set_profile(comm._h, 0)
         del g
     comm.check()
@@ -125,7 +139,10 @@ def main():
         res = {"world": world, "nodes": nodes, "dtype": args.dtype, "proto": args.proto,
                "calls": args.calls, "table": table, "best": best, "phases": phases,
                "phase_names": ["entry", "pdl_wait", "rs_pushed", "synced", "reduced+ag_pushed",
-                               "ag_received", "exit"]}
+                               "ag_received", "exit"],
+               "summary_names": ["release_spread", "median_cta_work", "last_exit",
+                                 "entry_to_release", "release_to_pushed", "pushed_to_synced",
+                                 "synced_to_reduced", "reduced_to_ag_received"]}
         line = json.dumps(res)
         print(line, flush=True)
         if args.out:
