@@ -317,6 +317,8 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   c->h_desc.node = c->rank / c->gpus;
   c->h_desc.local = c->rank % c->gpus;
   c->h_desc.timeout_ns = static_cast<uint64_t>(c->timeout_s * 1e9);
+  c->h_desc.poll_ns = 0;
+  if (const char* v = getenv("NVRAR_POLL_NS")) c->h_desc.poll_ns = static_cast<uint32_t>(atoi(v));
   c->h_desc.base[c->rank] = c->region;
   *out = c;
   return NVRAR_SUCCESS;

@@ -85,6 +85,7 @@ struct RankDesc {
   Layout lay;
   int rank, world, nodes, gpus, steps, node, local;
   int profile;
+  uint32_t poll_ns;  // back-off between unsatisfied polls (0 = spin)
   uint64_t timeout_ns;
 };
 
@@ -150,6 +151,7 @@ __device__ __forceinline__ uint32_t ld_volatile32(const void* p) {
 struct Ctl {
   RankState* st;
   uint64_t timeout_ns;
+  uint32_t poll_ns;
   uint32_t seq;
   uint32_t spins;
   uint64_t t0;
@@ -317,6 +319,7 @@ __device__ __forceinline__ void recv_unit(Ctl& c, uint4* slot, uint64_t u, uint3
       return;
     }
     if (wait_tick(c, kFlagWait, peer, u, bad)) return;
+    if (c.poll_ns) __nanosleep(c.poll_ns);
   }
   Pr::template clear<W>(slot, u);
 }

@@ -87,6 +87,7 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
   __syncthreads();
   c.st = d.state;
   c.timeout_ns = d.timeout_ns;
+  c.poll_ns = d.poll_ns;
   c.spins = 0;
   c.aborted = false;
   c.t0 = globaltimer();

@@ -64,8 +64,64 @@ def time_graph(g, reps, stream, local):
     return D.max_over_ranks(ts)
 
 
+def tune_emulated(args):
+    """Virtual ranks on one GPU (the N=1 bench workload): same sweep, no process group."""
+    from .comm import LocalGroup
+    nodes, gpus = args.emu_topo
+    p = nodes * gpus
+    g = LocalGroup(ClusterTopology(nodes, gpus), 8 << 20, device=0, timeout_s=30.0)
+    g.set_protocol(args.proto)
+    dt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    esz = 2 if dt == torch.bfloat16 else 4
+    stream = torch.cuda.Stream()
+    table, best = {}, {}
+    for size in [int(s) for s in args.sizes.split(",")]:
+        n = size // esz
+        nbuf = max(2, min(args.calls, (160 << 20) // (2 * size * p)))
+        bufs = [([torch.randn(n, device="cuda").to(dt) for _ in range(p)],
+                 [torch.empty(n, device="cuda", dtype=dt) for _ in range(p)]) for _ in range(nbuf)]
+        row = {}
+        for algo in ALGOS:
+            if algo == "oneshot" and size > (1 << 20):
+                continue
+            g.set_algo(algo)
+            for blocks in [int(b) for b in args.blocks.split(",")]:
+                if blocks * p > 148:
+                    continue
+                g.set_config(NvrarConfig(blocks, 65536))
+                gr = graph_of(lambda i: g.launch(*bufs[i % nbuf], stream=torch.cuda.current_stream()),
+                              args.calls, stream)
+                for _ in range(2):
+                    gr.replay()
+                torch.cuda.synchronize()
+                ts = []
+                for _ in range(args.reps):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    with torch.cuda.stream(stream):
+                        a.record(stream)
+                        gr.replay()
+                        b.record(stream)
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b))
+                row[f"{algo}/{blocks}"] = round(statistics.median(ts) * 1e3 / args.calls, 3)
+                del gr
+        g.check()
+        k = min(row, key=row.get)
+        table[str(size)] = row
+        best[str(size)] = [k.split("/")[0], int(k.split("/")[1]), row[k]]
+    res = {"world": 1, "emulated": f"{nodes}x{gpus}", "dtype": args.dtype, "proto": args.proto,
+           "table": table, "best": best}
+    line = json.dumps(res)
+    print(line, flush=True)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(line + "\n")
+    g.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--emu", default="", help="NxG: virtual ranks on one GPU instead of a process group")
     ap.add_argument("--sizes", default="65536,131072,262144,524288,1048576,2097152,4194304")
     ap.add_argument("--blocks", default="4,8,16,32,64,128")
     ap.add_argument("--nodes", type=int, default=0)
@@ -75,6 +131,10 @@ def main():
     ap.add_argument("--proto", default="auto")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
+    if args.emu:
+        args.emu_topo = tuple(int(v) for v in args.emu.split("x"))
+        tune_emulated(args)
+        return
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
