@@ -97,6 +97,14 @@ typedef enum {
  *   AUTO    — LAMPORT for float32/bf16, LL for int32. */
 typedef enum { NVRAR_PROTO_AUTO = 0, NVRAR_PROTO_LL = 1, NVRAR_PROTO_LAMPORT = 2 } nvrar_proto_t;
 
+/* One row of a measured selector table: messages of at most `max_bytes` run
+ * `algo` (HIER / TWOSHOT / ONESHOT) on `blocks` CTAs per rank. */
+typedef struct {
+  uint64_t max_bytes;
+  int algo;
+  int blocks;
+} nvrar_plan_entry;
+
 /* Bootstrap collective supplied by the caller for nvrar_init: gather `bytes`
  * from every rank into recv (rank-major). Return 0 on success. */
 typedef int (*nvrar_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
@@ -164,6 +172,11 @@ int nvrar_set_timeout(nvrar_comm_t comm, double timeout_s);
 int nvrar_set_protocol(nvrar_comm_t comm, nvrar_proto_t proto);
 /* Selected schedule and CTA count for a message (what nvrar_allreduce runs). */
 int nvrar_plan(nvrar_comm_t comm, size_t count, nvrar_dtype_t dtype, int* algo, int* blocks);
+/* Install a measured selector table (ascending max_bytes; messages larger than
+ * the last row fall back to the built-in policy). All ranks must install the
+ * same table — paper_2511_09557_b200.selector.autotune() measures it with a
+ * max-over-ranks consensus. n = 0 clears it. */
+int nvrar_set_plan_table(nvrar_comm_t comm, const nvrar_plan_entry* entries, int n);
 /* The same selector as a pure function (no device): every rank evaluates it
  * identically, which is what keeps all ranks on one schedule. */
 int nvrar_plan_for(int world, int nodes, int gpus_per_node, size_t count, nvrar_dtype_t dtype,

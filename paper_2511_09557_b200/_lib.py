@@ -58,6 +58,10 @@ class Handle(ctypes.Structure):
     _fields_ = [("bytes", ctypes.c_ubyte * HANDLE_BYTES)]
 
 
+class PlanEntry(ctypes.Structure):
+    _fields_ = [("max_bytes", ctypes.c_uint64), ("algo", ctypes.c_int), ("blocks", ctypes.c_int)]
+
+
 class Blocked(ctypes.Structure):
     _fields_ = [
         ("global_rank", ctypes.c_int),
@@ -88,6 +92,7 @@ SIGNATURES = {
     "nvrar_set_algo": (_c.c_int, [_vp, _c.c_int]),
     "nvrar_set_timeout": (_c.c_int, [_vp, _c.c_double]),
     "nvrar_set_protocol": (_c.c_int, [_vp, _c.c_int]),
+    "nvrar_set_plan_table": (_c.c_int, [_vp, _c.POINTER(PlanEntry), _c.c_int]),
     "nvrar_plan": (_c.c_int, [_vp, _c.c_size_t, _c.c_int, _c.POINTER(_c.c_int),
                               _c.POINTER(_c.c_int)]),
     "nvrar_plan_for": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_size_t, _c.c_int, _c.c_int,

@@ -82,6 +82,7 @@ struct nvrar_comm {
   int proto = NVRAR_PROTO_AUTO;
   uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
   uint64_t* d_scratch = nullptr;
+  std::vector<nvrar_plan_entry> table;  // measured selector (ascending max_bytes)
 };
 
 namespace {
@@ -173,44 +174,64 @@ int validate_args(const nvrar_init_args* a) {
 // function of its arguments, so every rank picks the same schedule. The
 // default policy is the measured one from the B200 sweep (DESIGN.md,
 // "selector"); user overrides (algo / blocks) win.
+// Default policy, from the B200 sweeps (paper_2511_09557_b200/tune.py; DESIGN.md
+// §selector): one-shot while the (P-1)·M inbound bytes stay small, the
+// hierarchical schedule in the middle (fewer wire bytes than one-shot, fewer
+// hops than two-shot at these P), two-shot for large messages; CTAs grow with
+// the message. `table` (from nvrar_set_plan_table, measured on the running
+// system) overrides it.
+void default_plan(int world, int nodes, uint64_t bytes, bool emu, int* algo, int* blocks) {
+  const uint64_t one_max = world <= 4 ? (512u << 10) : (256u << 10);
+  if (world == 1) {
+    *algo = NVRAR_ALGO_ONESHOT;
+  } else if (emu) {
+    *algo = NVRAR_ALGO_HIER;  // virtual ranks share one HBM: least traffic wins
+  } else if (bytes <= one_max) {
+    *algo = NVRAR_ALGO_ONESHOT;
+  } else if (bytes <= (2u << 20) && nodes > 1) {
+    *algo = NVRAR_ALGO_HIER;
+  } else {
+    *algo = NVRAR_ALGO_TWOSHOT;
+  }
+  if (bytes <= (256u << 10)) {
+    *blocks = 32;
+  } else if (bytes <= (512u << 10)) {
+    *blocks = 64;
+  } else {
+    *blocks = 128;
+  }
+}
+
 void plan_shape(int world, int nodes, int gpus, int algo_pref, int blocks_pref, int max_ctas,
-                uint64_t count, int dtype, int* algo, int* blocks) {
+                uint64_t count, int dtype, int* algo, int* blocks,
+                const std::vector<nvrar_plan_entry>* table = nullptr, bool emu = false) {
   const uint64_t bytes = count * dtype_bytes(dtype);
   const bool flat_ok = gpus <= flat_max_gpus(nodes) && world <= 16;
-  int a = algo_pref;
-  if (a == NVRAR_ALGO_AUTO) {
-    if (!flat_ok) {
-      a = NVRAR_ALGO_HIER;
-    } else if (world == 1 || bytes <= 64 * 1024) {
-      a = NVRAR_ALGO_ONESHOT;
-    } else {
-      a = NVRAR_ALGO_TWOSHOT;
+  int a = algo_pref, b = blocks_pref;
+  int da = NVRAR_ALGO_TWOSHOT, db = 32;
+  default_plan(world, nodes, bytes, emu, &da, &db);
+  if (table) {
+    for (const auto& e : *table) {
+      if (bytes <= e.max_bytes) {
+        da = e.algo;
+        db = e.blocks;
+        break;
+      }
     }
   }
+  if (a == NVRAR_ALGO_AUTO) a = da;
+  if (b <= 0) b = da == a ? db : std::max(db, 16);
   if ((a == NVRAR_ALGO_TWOSHOT || a == NVRAR_ALGO_ONESHOT) && !flat_ok) a = NVRAR_ALGO_HIER;
   if (a == NVRAR_ALGO_ONESHOT && bytes > kOneshotMaxBytes) a = NVRAR_ALGO_TWOSHOT;
-  uint64_t units;
-  if (a == NVRAR_ALGO_HIER) {
-    units = (((count + gpus - 1) / gpus) + 3) / 4;
-  } else if (a == NVRAR_ALGO_ONESHOT) {
-    units = (count + 3) / 4;
-  } else {
-    units = ((count + world - 1) / world + 3) / 4;
-  }
-  int b = blocks_pref;
-  if (b <= 0) {
-    // one unit per thread where possible, at least a few CTAs for NVLink injection
-    const uint64_t want = (units + kThreads - 1) / kThreads;
-    b = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(want, 4), 128));
-  }
   b = std::max(1, std::min(b, max_ctas));
   *algo = a;
   *blocks = b;
 }
 
-void plan(const nvrar_comm* c, uint64_t count, int dtype, int* algo, int* blocks) {
+void plan(const nvrar_comm* c, uint64_t count, int dtype, int* algo, int* blocks,
+          bool emu = false) {
   plan_shape(c->world, c->nodes, c->gpus, c->algo, c->blocks, c->max_ctas, count, dtype, algo,
-             blocks);
+             blocks, c->table.empty() ? nullptr : &c->table, emu);
 }
 
 int check_sticky(nvrar_comm* c) {
@@ -498,6 +519,20 @@ int nvrar_plan(nvrar_comm_t c, size_t count, nvrar_dtype_t dtype, int* algo, int
   return NVRAR_SUCCESS;
 }
 
+int nvrar_set_plan_table(nvrar_comm_t c, const nvrar_plan_entry* entries, int n) {
+  if (!c || n < 0 || (n > 0 && !entries)) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad table");
+  std::vector<nvrar_plan_entry> t(entries, entries + n);
+  for (int i = 0; i < n; ++i) {
+    if (t[i].algo < NVRAR_ALGO_HIER || t[i].algo > NVRAR_ALGO_ONESHOT || t[i].blocks < 1 ||
+        (i > 0 && t[i].max_bytes <= t[i - 1].max_bytes)) {
+      return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                  "plan table entry %d: need ascending max_bytes, a concrete algo, blocks >= 1", i);
+    }
+  }
+  c->table = std::move(t);
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_plan_for(int world, int nodes, int gpus, size_t count, nvrar_dtype_t dtype,
                    int algo_pref, int blocks_pref, int max_ctas, int* algo, int* blocks) {
   if (!algo || !blocks || world != nodes * gpus || !is_pow2(nodes) || max_ctas < 1) {
@@ -562,7 +597,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
     return NVRAR_SUCCESS;
   }
   int algo = 0, blocks = 1;
-  plan(c0, count, dtype, &algo, &blocks);
+  plan(c0, count, dtype, &algo, &blocks, local_group && nl > 1);
   const bool emu = local_group;
   if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
