@@ -86,6 +86,42 @@ def main():
     torch.cuda.synchronize()
     res["launch_floor_us"] = a.elapsed_time(b) * 1e3 / 100
 
+    # copy floor: a 1x1 communicator (the same kernel, no peers) in a graph —
+    # launch + input load + output store + grid completion, per call
+    solo = Communicator(ClusterTopology(1, 1), 0, local, 8 << 20)
+    solo.connect([solo.export()])
+    floors = {}
+    for size in (128 << 10, 1 << 20):
+        xs = [(torch.randn(size // 2, device="cuda").to(torch.bfloat16),
+               torch.empty(size // 2, device="cuda", dtype=torch.bfloat16)) for _ in range(80)]
+        solo._lib.nvrar_set_profile(solo._h, 1)
+        s2 = torch.cuda.Stream()
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s2):
+            solo.allreduce(*xs[0])
+        torch.cuda.current_stream().wait_stream(s2)
+        torch.cuda.synchronize()
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=s2):
+            for i in range(80):
+                solo.allreduce(*xs[i])
+        g2.replay()
+        torch.cuda.synchronize()
+        a.record()
+        g2.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts = (ctypes.c_uint64 * 8)()
+        solo._lib.nvrar_get_phase_times(solo._h, ts, 8)
+        floors[f"{size >> 10}KB"] = {
+            "per_call_us": round(a.elapsed_time(b) * 1e3 / 80, 3),
+            "cta0_release_to_exit_us": round((ts[6] - ts[7]) / 1e3, 3),
+            "cta0_release_to_loaded_us": round((ts[2] - ts[7]) / 1e3, 3),
+            "entry_to_release_us": round((ts[7] - ts[0]) / 1e3, 3)}
+        del g2
+    solo.close()
+    res["copy_floor_p1"] = floors
+
     # phase breakdown of single calls
     comm._lib.nvrar_set_profile(comm._h, 1)
     phases = {}
