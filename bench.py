@@ -1,6 +1,7 @@
-"""NVRAR all-reduce benchmark (driver contract; see DESIGN.md §Measurement).
+"""NVRAR all-reduce benchmark (driver contract; see DESIGN.md §6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nvrar|reference]
+                    [--no-sweep] [--no-autotune]
 
 N=1  : BASELINE configs[0] on one B200 — 8 ranks as 2 virtual nodes x 4, 1 MB
        fp32 sum; the 8 ranks are virtual ranks on cuda:0 (one cooperative
@@ -9,6 +10,8 @@ N=1  : BASELINE configs[0] on one B200 — 8 ranks as 2 virtual nodes x 4, 1 MB
 N>1  : launched by torch.distributed.run, one rank per GPU; hierarchy 2 x N/2
        (N=8: 2x4, configs[1]); headline message 1 MB bf16, plus the 64 KB-8 MB
        sweep against NCCL all-reduce on the same buffers (configs[1]/[2]).
+       The selector is first tuned on the running box (max-over-ranks
+       consensus), as the north star's measured selector.
 
 A "step" is one CUDA-graph replay of `calls` back-to-back all-reduces over
 rotating buffers whose total exceeds the 126 MB L2 (so no call reads an input
@@ -23,19 +26,15 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-L2_BYTES = 126 << 20
-ROTATE_BYTES = 160 << 20   # > L2: rotating input+output footprint per GPU
 METRIC = "all-reduce p50 latency (µs, max over ranks) 128KB–2MB at 2/4/8 B200 vs NCCL"
-NVLINK_PEAK_GBS = 770.0    # measured peer copy per direction (B200_PROFILING.md); 900 nominal
-NVLINK_NOMINAL_GBS = 900.0
+NVLINK_PEAK_GBS = 770.0     # measured B200 peer copy per direction (B200_PROFILING.md)
+NVLINK_NOMINAL_GBS = 900.0  # NVLink 5 per direction per GPU
 SWEEP = [64 << 10, 128 << 10, 256 << 10, 512 << 10, 1 << 20, 2 << 20, 4 << 20, 8 << 20]
 
 
@@ -48,115 +47,23 @@ def peaks():
         return 6650.0, "fallback"
 
 
-# ---- clocks sampled during the timed region --------------------------------------
-
-class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
-        self.index = index
-        self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
-
-    def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        return self
-
-    def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
-
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
-                    "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
-
-
-# ---- graph timing -------------------------------------------------------------------
-
-def graph_of(torch, fn, calls, stream):
-    """Capture `calls` back-to-back invocations fn(i) into one CUDA graph."""
-    stream.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(stream):
-        for i in range(min(calls, 4)):
-            fn(i)
-    torch.cuda.current_stream().wait_stream(stream)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=stream):
-        for i in range(calls):
-            fn(i)
-    torch.cuda.synchronize()
-    return g
-
-
-def time_steps(torch, replay, steps, warmup, barrier, stream):
-    """Per-step device time (ms) of `replay()` with events on `stream`."""
-    for _ in range(warmup):
-        with torch.cuda.stream(stream):
-            replay()
-    torch.cuda.synchronize()
-    times = []
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(steps)]
-    barrier()
-    torch.cuda.synchronize()
-    with torch.cuda.stream(stream):
-        for a, b in ev:
-            a.record(stream)
-            replay()
-            b.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    for a, b in ev:
-        times.append(a.elapsed_time(b))
-    return times
-
-
-# ---- the CPU reference path ---------------------------------------------------------
+# ---- the CPU reference path (the reference's own code, compiled in oracle/_ref) -------
 
 def cpu_reference(nodes, gpus, n, budget_s=12.0, max_calls=60):
-    """ccsim::NvrarAllreduce<float> on the reference's ConcurrentEngine (oracle/_ref,
-    compiled from the reference sources), pre-generated inputs, per-call makespan."""
+    """ccsim::NvrarAllreduce<float> on the reference's ConcurrentEngine, pre-generated
+    inputs, per-call makespan (bench.hpp:116-122 convention)."""
     from oracle import oracle as O
     x = O.random_inputs(nodes * gpus, n, 1234, "f32")
     kind = "reference" if O.ref_available() else "port"
     if kind == "port":
         # the C restatement (single thread) of the same arithmetic
         t0 = time.perf_counter()
-        calls = 0
         per = []
-        while calls < max_calls and time.perf_counter() - t0 < budget_s:
+        while len(per) < max_calls and time.perf_counter() - t0 < budget_s:
             t = time.perf_counter()
             O.nvrar_order_sum(x, nodes, gpus)
             per.append((time.perf_counter() - t) * 1e6)
-            calls += 1
-        return statistics.median(per), kind, 1, f"{calls} calls, {nodes}x{gpus}, n={n} fp32"
+        return statistics.median(per), kind, 1, f"{len(per)} calls, {nodes}x{gpus}, n={n} fp32"
     t0 = time.perf_counter()
     per = list(O.ref_time_concurrent(x, nodes, gpus, warmup=2, calls=3))
     one = (time.perf_counter() - t0) / 5
@@ -168,8 +75,6 @@ def cpu_reference(nodes, gpus, n, budget_s=12.0, max_calls=60):
             f"{len(per)} calls of NvrarAllreduce<float> on ConcurrentEngine, {nodes}x{gpus}, "
             f"n={n} fp32, B=1, C=65536, p50 of per-call makespan (host nproc={os.cpu_count()})")
 
-
-# ---- arms ---------------------------------------------------------------------------------
 
 def hier_for(world):
     return {1: (2, 4), 2: (2, 1), 4: (2, 2), 8: (2, 4)}[world]
@@ -184,6 +89,7 @@ def run_reference(args, rank, world):
     t0 = time.perf_counter()
     for _ in range(args.warmup):
         cpu_reference(nodes, gpus, n, budget_s=2.0, max_calls=3)
+    kind, cores, sample = "reference", nodes * gpus, ""
     for _ in range(args.steps):
         v, kind, cores, sample = cpu_reference(nodes, gpus, n, budget_s=4.0, max_calls=10)
         per.append(v)
@@ -206,49 +112,51 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def calls_for(msg_bytes, ranks_on_gpu):
-    per_call = 2 * msg_bytes * ranks_on_gpu
-    return int(min(1000, max(50, math.ceil(ROTATE_BYTES / per_call))))
-
+# ---- N = 1: configs[0] with 8 virtual ranks on cuda:0 ----------------------------------
 
 def run_emulated(args):
-    """N=1: configs[0] with 8 virtual ranks on cuda:0."""
     import numpy as np
     import torch
 
     from oracle import oracle as O
     from paper_2511_09557_b200 import ClusterTopology, LocalGroup, NvrarConfig
-    from paper_2511_09557_b200 import _lib as L
+    from paper_2511_09557_b200 import harness as H
 
     nodes, gpus = 2, 4
     P = nodes * gpus
     msg = 1 << 20
     n = msg // 4
-    calls = calls_for(msg, P)
-    g = LocalGroup(ClusterTopology(nodes, gpus), max(msg, 8 << 20), device=0, timeout_s=30.0)
-    algo, blocks = g.comms[0].plan(n, torch.float32)
+    calls = H.calls_for(msg, P)
+    g = LocalGroup(ClusterTopology(nodes, gpus), 8 << 20, device=0, timeout_s=30.0)
     x = O.random_inputs(P, n, 1234, "f32")
     base_in = [torch.from_numpy(x[r]).cuda() for r in range(P)]
-    sets = []
-    for _ in range(calls):
-        ins = [t.clone() for t in base_in]
-        outs = [torch.empty_like(t) for t in base_in]
-        sets.append((ins, outs))
+    sets = [([t.clone() for t in base_in], [torch.empty_like(t) for t in base_in])
+            for _ in range(calls)]
     stream = torch.cuda.Stream()
 
-    def call(i):
-        ins, outs = sets[i]
-        g.launch(ins, outs, stream=torch.cuda.current_stream())
+    def graph_for():
+        return H.graph_of(lambda i: g.launch(*sets[i], stream=torch.cuda.current_stream()),
+                          calls, stream)
 
-    graph = graph_of(torch, call, calls, stream)
+    # the selector's choice for this shape, and each schedule forced (context)
+    by_algo = {}
+    for algo in ("hier", "twoshot", "oneshot"):
+        g.set_algo(algo)
+        gr = graph_for()
+        ts = H.time_replays(gr.replay, max(3, args.steps // 2), 2, lambda: None, stream)
+        by_algo[algo] = round(statistics.median(ts) * 1e3 / calls, 3)
+        del gr
+    g.set_algo("auto")
+    algo, blocks = g.comms[0].plan(n, torch.float32)
+    graph = graph_for()
     hbm, hbm_kind = peaks()
-    with ClockSampler(0) as clk:
-        times = time_steps(torch, graph.replay, args.steps, args.warmup, lambda: None, stream)
+    with H.ClockSampler(0) as clk:
+        times = H.time_replays(graph.replay, args.steps, args.warmup, lambda: None, stream)
     g.check()
     want = O.nvrar_order_sum(x, nodes, gpus).view(np.uint32)
     for r in range(P):
         assert np.array_equal(sets[-1][1][r].cpu().numpy().view(np.uint32), want), "parity"
-    per_call_us = [t * 1e3 / calls for t in times]
+    per_call_us = sorted(t * 1e3 / calls for t in times)
     p50 = statistics.median(per_call_us)
     # roofline: every rank's input read + output written once from HBM (2*P*M)
     alg_bytes = 2 * P * msg
@@ -276,17 +184,16 @@ def run_emulated(args):
     g.check()
     assert np.array_equal(host_out[0].numpy().view(np.uint32), want)
 
-    # bf16 sweep on the same virtual group (context for the configs[1] sizes)
     sweep = {}
     if not args.no_sweep:
         for size in (128 << 10, 512 << 10, 2 << 20):
             ne = size // 2
-            c2 = calls_for(size, P)
+            c2 = H.calls_for(size, P)
             xs = [torch.randn(ne, device="cuda").to(torch.bfloat16) for _ in range(P)]
             st = [([t.clone() for t in xs], [torch.empty_like(t) for t in xs]) for _ in range(c2)]
-            gr = graph_of(torch, lambda i: g.launch(*st[i], stream=torch.cuda.current_stream()),
-                          c2, stream)
-            ts = time_steps(torch, gr.replay, max(5, args.steps // 2), 2, lambda: None, stream)
+            gr = H.graph_of(lambda i: g.launch(*st[i], stream=torch.cuda.current_stream()),
+                            c2, stream)
+            ts = H.time_replays(gr.replay, max(5, args.steps // 2), 2, lambda: None, stream)
             sweep[f"{size >> 10}KB_bf16"] = {"p50_us": round(statistics.median(ts) * 1e3 / c2, 3),
                                              "algo": g.comms[0].plan(ne, torch.bfloat16)[0]}
             del gr, st
@@ -303,14 +210,14 @@ def run_emulated(args):
                                "B200, one cooperative launch per all-reduce), 1 MB fp32 sum",
                    "nodes": nodes, "gpus_per_node": gpus, "message_bytes": msg, "algo": algo,
                    "blocks_per_rank": blocks, "calls_per_step": calls,
+                   "per_schedule_us": by_algo,
                    "l2": f"rotating buffers, {calls} x 16 MB per step > 126 MB L2",
-                   "p10_us": round(sorted(per_call_us)[len(per_call_us) // 10], 3),
-                   "p90_us": round(sorted(per_call_us)[(9 * len(per_call_us)) // 10], 3)},
+                   "p10_us": round(per_call_us[len(per_call_us) // 10], 3),
+                   "p90_us": round(per_call_us[(9 * len(per_call_us)) // 10], 3)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "peak_kind": hbm_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "traffic": None,
-                     "algorithmic_bytes": alg_bytes,
-                     "note": "emulated ranks share one HBM: 2*P*M bytes (all inputs read, all "
+                     "traffic": None, "algorithmic_bytes": alg_bytes,
+                     "note": "virtual ranks share one HBM: 2*P*M bytes (all inputs read, all "
                              "outputs written) per launch"},
         "cpu_baseline": {"value": round(cpu_v, 3), "unit": "us", "cores": cpu_cores,
                          "kind": cpu_kind, "sample": cpu_sample},
@@ -324,13 +231,16 @@ def run_emulated(args):
     g.close()
 
 
+# ---- N > 1: one rank per GPU over NVLink ----------------------------------------------
+
 def run_multi(args, rank, world, local):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2511_09557_b200 import ClusterTopology, Communicator
     from paper_2511_09557_b200 import dist as D
+    from paper_2511_09557_b200 import harness as H
+    from paper_2511_09557_b200 import selector as S
 
     torch.cuda.set_device(local)
     os.environ.setdefault("NCCL_DEBUG", "WARN")
@@ -340,36 +250,42 @@ def run_multi(args, rank, world, local):
                                            timeout_s=30.0)
     stream = torch.cuda.Stream()
     barrier = lambda: dist.barrier(device_ids=[local])  # noqa: E731
+    dev = torch.device("cuda", local)
 
-    def measure(msg, dtype, impl, steps, warmup, algo="auto"):
-        ne = msg // (2 if dtype == torch.bfloat16 else 4)
-        calls = calls_for(msg, 1)
+    alpha = H.alpha_signal_us(comm, rank, world)
+    tuned = None
+    if not args.no_autotune:
+        tuned = S.autotune(comm, sizes=SWEEP, dtype=torch.bfloat16, calls=30, reps=5)
+
+    def measure(msg, impl, steps, warmup):
+        ne = msg // 2
+        calls = H.calls_for(msg, 1)
         torch.manual_seed(1234 + rank)
-        src = torch.randn(ne, device="cuda").to(dtype)
+        src = torch.randn(ne, device="cuda").to(torch.bfloat16)
         bufs = [(src.clone(), torch.empty_like(src)) for _ in range(calls)]
         if impl == "nvrar":
-            comm.set_algo(algo)
-            plan = D.plan_consensus(comm.plan(ne, dtype))
+            plan = D.plan_consensus(comm.plan(ne, torch.bfloat16))
             fn = lambda i: comm.allreduce(bufs[i][0], bufs[i][1])  # noqa: E731
         else:
             plan = ("nccl", 0)
             fn = lambda i: dist.all_reduce(bufs[i][1])  # noqa: E731
             for a, b in bufs:
                 b.copy_(a)
-        gr = graph_of(torch, fn, calls, stream)
-        ts = time_steps(torch, gr.replay, steps, warmup, barrier, stream)
-        ts = D.max_over_ranks(ts, device=torch.device("cuda", local))
+        gr = H.graph_of(fn, calls, stream)
+        ts = H.time_replays(gr.replay, steps, warmup, barrier, stream)
+        ts = D.max_over_ranks(ts, device=dev)
         if impl == "nvrar":
             comm.check()
         del gr
-        per = [t * 1e3 / calls for t in ts]
-        return statistics.median(per), per, calls, plan
+        return sorted(t * 1e3 / calls for t in ts), calls, plan
 
-    hbm, hbm_kind = peaks()
+    hbm, _ = peaks()
     msg = 1 << 20
-    with ClockSampler(local) as clk:
-        p50, per, calls, plan = measure(msg, torch.bfloat16, "nvrar", args.steps, args.warmup)
-    nccl50, _, _, _ = measure(msg, torch.bfloat16, "nccl", args.steps, args.warmup)
+    with H.ClockSampler(local) as clk:
+        per, calls, plan = measure(msg, "nvrar", args.steps, args.warmup)
+    p50 = statistics.median(per)
+    nccl_per, _, _ = measure(msg, "nccl", args.steps, args.warmup)
+    nccl50 = statistics.median(nccl_per)
 
     # e2e: pinned host input -> device, all-reduce, device -> host, per step; max over ranks
     ne = msg // 2
@@ -377,7 +293,6 @@ def run_multi(args, rank, world, local):
     host_out = torch.empty(ne, dtype=torch.bfloat16).pin_memory()
     din = torch.empty(ne, dtype=torch.bfloat16, device="cuda")
     dout = torch.empty_like(din)
-    comm.set_algo("auto")
     e2e = []
     for k in range(args.warmup + args.steps):
         barrier()
@@ -391,29 +306,36 @@ def run_multi(args, rank, world, local):
         b.synchronize()
         if k >= args.warmup:
             e2e.append(a.elapsed_time(b) * 1e3)
-    e2e = D.max_over_ranks(e2e, device=torch.device("cuda", local))
+    e2e = D.max_over_ranks(e2e, device=dev)
     comm.check()
+
+    def roof_us(size):
+        b_alg = 2 * (world - 1) / world * size
+        bw = b_alg / (NVLINK_NOMINAL_GBS * 1e9) * 1e6
+        lat = math.log2(world) * alpha if alpha else 0.0
+        return max(bw, lat), b_alg
 
     sweep = {}
     if not args.no_sweep:
         for size in SWEEP:
             s_steps = max(5, args.steps // 2)
-            v, _, _, pl = measure(size, torch.bfloat16, "nvrar", s_steps, 2)
-            nv, _, _, _ = measure(size, torch.bfloat16, "nccl", s_steps, 2)
+            v_per, _, pl = measure(size, "nvrar", s_steps, 2)
+            n_per, _, _ = measure(size, "nccl", s_steps, 2)
+            v, nv = statistics.median(v_per), statistics.median(n_per)
+            rt, b_alg = roof_us(size)
             row = {"nvrar_us": round(v, 3), "nccl_us": round(nv, 3), "algo": pl[0],
-                   "blocks": pl[1], "speedup_vs_nccl": round(nv / v, 3)}
-            for forced in ("hier", "twoshot", "oneshot"):
-                if forced == "oneshot" and size > (1 << 20):
-                    continue
-                fv, _, _, _ = measure(size, torch.bfloat16, "nvrar", s_steps, 2, algo=forced)
-                row[f"{forced}_us"] = round(fv, 3)
-            b_alg = 2 * (world - 1) / world * size
-            row["busbw_GBs"] = round(b_alg / (v * 1e-6) / 1e9, 1)
-            row["bw_floor_us"] = round(b_alg / (NVLINK_NOMINAL_GBS * 1e9) * 1e6, 3)
+                   "blocks": pl[1], "speedup_vs_nccl": round(nv / v, 3),
+                   "busbw_GBs": round(b_alg / (v * 1e-6) / 1e9, 1),
+                   "roofline_us": round(rt, 3), "roofline_frac": round(rt / v, 3)}
+            if tuned is not None:
+                cands = tuned["measured"][size]
+                for a_name in ("hier", "twoshot", "oneshot"):
+                    vals = [t for k, t in cands.items() if k.startswith(a_name + "/")]
+                    if vals:
+                        row[f"{a_name}_best_us"] = min(vals)
             sweep[f"{size >> 10}KB"] = row
-            comm.set_algo("auto")
 
-    b_alg = 2 * (world - 1) / world * msg
+    rt, b_alg = roof_us(msg)
     busbw = b_alg / (p50 * 1e-6) / 1e9
     if rank == 0:
         line = {
@@ -426,15 +348,21 @@ def run_multi(args, rank, world, local):
                                    f"nodes, 1 MB message (configs[1] sweep point)",
                        "nodes": nodes, "gpus_per_node": gpus, "message_bytes": msg,
                        "algo": plan[0], "blocks_per_rank": plan[1], "calls_per_step": calls,
+                       "selector": "autotuned on this box" if tuned else "built-in policy",
+                       "selector_rows": tuned["rows"] if tuned else None,
                        "l2": f"rotating buffers, {calls} x 2 MB per step > 126 MB L2",
+                       "p10_us": round(per[len(per) // 10], 3),
+                       "p90_us": round(per[(9 * len(per)) // 10], 3),
                        "nccl_p50_us": round(nccl50, 3),
-                       "speedup_vs_nccl": round(nccl50 / p50, 3)},
+                       "speedup_vs_nccl": round(nccl50 / p50, 3),
+                       "alpha_signal_us": round(alpha, 3) if alpha else None},
             "roofline": {"bound": "nvlink", "achieved": round(busbw, 1),
                          "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                          "frac": round(busbw / NVLINK_PEAK_GBS, 4), "traffic": None,
                          "algorithmic_bytes": b_alg,
-                         "note": "busbw = 2(P-1)/P*M / t (nccl-tests convention); peak = measured "
-                                 "B200 peer copy per direction (900 nominal)"},
+                         "roofline_us": round(rt, 3), "time_frac": round(rt / p50, 4),
+                         "note": "achieved = busbw 2(P-1)/P*M/t vs measured 770 GB/s peer copy; "
+                                 "roofline_us = max(B_alg/900 GB/s, log2(P)*alpha_signal)"},
             "cpu_baseline": None,
             "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
                     "h2d_bytes_per_step": msg, "d2h_bytes_per_step": msg},
@@ -455,6 +383,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["nvrar", "reference"], default="nvrar")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-autotune", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
