@@ -5,6 +5,7 @@
 //   ./tools/launch_micro
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <vector>
