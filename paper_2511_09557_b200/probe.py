@@ -91,10 +91,13 @@ def main():
     solo = Communicator(ClusterTopology(1, 1), 0, local, 8 << 20)
     solo.connect([solo.export()])
     floors = {}
-    for size in (128 << 10, 1 << 20):
+    from .comm import NvrarConfig
+    for size, blocks, prof in ((128 << 10, 32, 1), (128 << 10, 32, 0), (128 << 10, 4, 0),
+                               (128 << 10, 128, 0), (1 << 20, 32, 1), (1 << 20, 128, 0)):
+        solo.set_config(NvrarConfig(blocks, 65536))
         xs = [(torch.randn(size // 2, device="cuda").to(torch.bfloat16),
                torch.empty(size // 2, device="cuda", dtype=torch.bfloat16)) for _ in range(80)]
-        solo._lib.nvrar_set_profile(solo._h, 1)
+        solo._lib.nvrar_set_profile(solo._h, prof)
         s2 = torch.cuda.Stream()
         s2.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s2):
@@ -113,7 +116,7 @@ def main():
         torch.cuda.synchronize()
         ts = (ctypes.c_uint64 * 8)()
         solo._lib.nvrar_get_phase_times(solo._h, ts, 8)
-        floors[f"{size >> 10}KB"] = {
+        floors[f"{size >> 10}KB_b{blocks}_prof{prof}"] = {
             "per_call_us": round(a.elapsed_time(b) * 1e3 / 80, 3),
             "cta0_release_to_exit_us": round((ts[6] - ts[7]) / 1e3, 3),
             "cta0_release_to_loaded_us": round((ts[2] - ts[7]) / 1e3, 3),
