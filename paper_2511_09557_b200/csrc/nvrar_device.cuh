@@ -111,35 +111,39 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Data-path accesses carry no "memory" clobber: cells are self-validating, so
+// no ordering against unrelated loads/stores is needed, and leaving the
+// compiler free to hoist the next unit's input loads above this unit's remote
+// stores is what keeps several HBM loads in flight per thread. (asm volatile
+// statements still keep their order among themselves: read-then-empty of a
+// cell stays in program order. pdl_wait keeps its clobber.)
 __device__ __forceinline__ uint4 ld_volatile16(const void* p) {
   uint4 v;
   asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
+               : "l"(p));
   return v;
 }
 
 __device__ __forceinline__ void st_volatile16(void* p, uint32_t a, uint32_t b, uint32_t c,
                                               uint32_t d) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b),
-               "r"(c), "r"(d)
-               : "memory");
+               "r"(c), "r"(d));
 }
 
 __device__ __forceinline__ uint64_t ld_volatile64(const void* p) {
   uint64_t v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
 
 __device__ __forceinline__ void st_volatile64(void* p, uint64_t v) {
-  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
 
 __device__ __forceinline__ uint32_t ld_volatile32(const void* p) {
   uint32_t v;
-  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 

@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       const int cc = (local + j) % G;
       uint4* slot = slot_a(d, node * G + cc, parity, local);
       const uint64_t cbase = static_cast<uint64_t>(cc) * S;
+#pragma unroll 4
       for (uint64_t u = u_first + blockDim.x; u < ue; u += blockDim.x) {
         const int valid = chunk_valid<UE>(S, u, n, cbase);
         if (valid == 0) continue;  // pure padding: skipped identically by the reader
@@ -445,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     const int q = (me + j) % P;
     const uint64_t qbase = oneshot ? 0 : static_cast<uint64_t>(q) * SP;
     uint4* slot = slot_a(d, q, parity, me);
+#pragma unroll 4
     for (uint64_t u = (j < kPre ? u_first + blockDim.x : u_first); u < ue; u += blockDim.x) {
       const uint64_t e = qbase + UE * u;
       const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e));

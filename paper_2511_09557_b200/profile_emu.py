@@ -22,9 +22,25 @@ def main():
     ap.add_argument("--nodes", type=int, default=2)
     ap.add_argument("--gpus", type=int, default=4)
     ap.add_argument("--proto", default="auto")
+    ap.add_argument("--solo", action="store_true",
+                    help="one 1x1 communicator (the single-rank kernel, no virtual ranks)")
+    ap.add_argument("--blocks", type=int, default=0)
     args = ap.parse_args()
     dt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     n = args.bytes // (4 if args.dtype == "f32" else 2)
+    if args.solo:
+        from .comm import Communicator, NvrarConfig
+        c = Communicator(ClusterTopology(1, 1), 0, 0, max(args.bytes, 1 << 20))
+        c.connect([c.export()])
+        c.set_config(NvrarConfig(args.blocks, 65536))
+        x = torch.randn(n, device="cuda").to(dt)
+        y = torch.empty_like(x)
+        for _ in range(args.calls):
+            c.allreduce(x, y)
+        c.check()
+        print("solo plan", c.plan(n, dt), "ok")
+        c.close()
+        return
     p = args.nodes * args.gpus
     g = LocalGroup(ClusterTopology(args.nodes, args.gpus), max(args.bytes, 1 << 20), device=0)
     g.set_algo(args.algo)
