@@ -80,6 +80,7 @@ struct nvrar_comm {
   int max_ctas = 148;  // co-resident CTAs of one kernel on this device
   bool pdl = true;     // programmatic dependent launch for single-rank launches
   int proto = NVRAR_PROTO_AUTO;
+  int threads = kThreads;  // threads per CTA (multiple of 32, <= kThreads)
   uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
   uint64_t* d_scratch = nullptr;
   std::vector<nvrar_plan_entry> table;  // measured selector (ascending max_bytes)
@@ -323,6 +324,10 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   }
   c->max_ctas = std::max(1, std::min(kSeqSlots, sms * std::max(occ, 1)));
   if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
+  if (const char* v = getenv("NVRAR_THREADS")) {
+    const int t = atoi(v);
+    if (t >= 32 && t <= kThreads && t % 32 == 0) c->threads = t;
+  }
   if (const char* v = getenv("NVRAR_PROTO")) {
     c->proto = std::string(v) == "ll" ? NVRAR_PROTO_LL
                : std::string(v) == "lamport" ? NVRAR_PROTO_LAMPORT : NVRAR_PROTO_AUTO;
@@ -608,7 +613,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(blocks, nl);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(c0->threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
   void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
   const uint64_t u_first = ub + threadIdx.x;
+  // grp[j] = (local + j) % G for j < G, without a division per use
+  int grp[kHierMaxG];
+#pragma unroll
+  for (int j = 0; j < kHierMaxG; ++j) grp[j] = local + j >= G ? local + j - G : local + j;
 
   begin_wait(d);
   // Prefetch this thread's first unit of every chunk before the call number is
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   for (int j = 0; j < kHierMaxG; ++j) {
     pv[j] = 0;
     if (j < G && u_first < ue) {
-      const uint64_t cbase = static_cast<uint64_t>((local + j) % G) * S;
+      const uint64_t cbase = static_cast<uint64_t>(grp[j]) * S;
       pv[j] = chunk_valid<UE>(S, u_first, n, cbase);
       if (pv[j] > 0) load_raw<E, UE>(send, cbase + UE * u_first, pv[j], pre[j]);
     }
@@ -197,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
     for (int j = 1; j < kHierMaxG; ++j) {
       if (j < G && pv[j] > 0) {
-        Raw::template put<RDW>(slot_a(d, node * G + (local + j) % G, parity, local), u_first,
+        Raw::template put<RDW>(slot_a(d, node * G + grp[j], parity, local), u_first,
                                pre[j], c.seq);
       }
     }
@@ -257,15 +261,15 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G) {
-          ok[j - 1] = Raw::template try_get<RDW>(slot_a(d, me, parity, (local + j) % G), uu[k],
+          ok[j - 1] = Raw::template try_get<RDW>(slot_a(d, me, parity, grp[j]), uu[k],
                                                  c.seq, r[j - 1], bad);
-          if (ok[j - 1]) Raw::template clear<RDW>(slot_a(d, me, parity, (local + j) % G), uu[k]);
+          if (ok[j - 1]) Raw::template clear<RDW>(slot_a(d, me, parity, grp[j]), uu[k]);
         }
       }
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G && !ok[j - 1]) {
-          const int s = (local + j) % G;
+          const int s = grp[j];
           recv_unit<Raw, RDW>(c, slot_a(d, me, parity, s), uu[k], r[j - 1], node * G + s);
         }
       }
@@ -318,9 +322,11 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       uint32_t o[RDW];
       acc_to_raw<UE>(E{}, f[k], o);
       store_raw<E, UE>(recv, mybase + UE * uu[k], valid[k], o);
-      for (int j = 1; j < G; ++j) {
-        Raw::template put<RDW>(slot_b(d, node * G + (local + j) % G, parity, local), uu[k], o,
-                               c.seq);
+#pragma unroll
+      for (int j = 1; j < kHierMaxG; ++j) {
+        if (j < G) {
+          Raw::template put<RDW>(slot_b(d, node * G + grp[j], parity, local), uu[k], o, c.seq);
+        }
       }
     }
   }
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G) {
-          const int s = (local + j) % G;
+          const int s = grp[j];
           valid[j - 1] = chunk_valid<UE>(S, u, n, static_cast<uint64_t>(s) * S);
           ok[j - 1] = valid[j - 1] == 0;
           if (!ok[j - 1]) {
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
         if (j < G) {
-          const int s = (local + j) % G;
+          const int s = grp[j];
           if (!ok[j - 1]) recv_unit<Raw, RDW>(c, slot_b(d, me, parity, s), u, r[j - 1], node * G + s);
           if (valid[j - 1] > 0) {
             store_raw<E, UE>(recv, static_cast<uint64_t>(s) * S + UE * u, valid[j - 1], r[j - 1]);
@@ -464,35 +470,48 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   __syncthreads();
   stamp(d, 3);
 
-  const uint64_t mybase = oneshot ? 0 : static_cast<uint64_t>(me) * SP;
+  // Index math in 32 bits (counts < 2^31 elements) and slot bases hoisted out
+  // of the unit loop: per unit the kernel does one division (the shard of the
+  // unit's first element) and walks the fold order incrementally.
+  const uint32_t mybase = oneshot ? 0u : static_cast<uint32_t>(me * SP);
+  const uint32_t n32 = static_cast<uint32_t>(n), SG32 = static_cast<uint32_t>(SG);
+  uint8_t* const a_mine = d.base[me] + d.lay.a_off + static_cast<uint64_t>(parity) * d.world * d.lay.a_src * 8;
+  const uint64_t a_stride = d.lay.a_src * 8;
   for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-    const uint64_t e0 = mybase + UE * u;
-    const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+    const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);
+    const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
     if (valid == 0) continue;
-    const int c0 = static_cast<int>(e0 / SG);
-    const int c3 = static_cast<int>((e0 + valid - 1) / SG);
+    const int c0 = static_cast<int>(e0 / SG32);
+    const bool straddle = e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32;
+    int l0 = c0 + 1;
+    if (l0 >= G) l0 -= G;
 
     // Every source's unit, in fold order relative to c0: r[nn][j] is the copy
     // of local rank (c0+1+j) % G of node nn.
     uint32_t r[N][MAXG][RDW];
     bool ok[N][MAXG];
+    int src[N][MAXG];
     uint32_t bad = 0;
 #pragma unroll
     for (int nn = 0; nn < N; ++nn) {
+      int l = l0;
 #pragma unroll
       for (int j = 0; j < MAXG; ++j) {
         ok[nn][j] = true;
+        src[nn][j] = nn * G + l;
         if (j < G) {
-          const int s = nn * G + (c0 + 1 + j) % G;
+          const int s = src[nn][j];
           if (s == me && u == u_first) {
 #pragma unroll
             for (int q = 0; q < RDW; ++q) r[nn][j][q] = pre[0][q];
           } else if (s == me) {
             load_raw<E, UE>(send, e0, valid, r[nn][j]);
           } else {
-            ok[nn][j] = Raw::template try_get<RDW>(slot_a(d, me, parity, s), u, c.seq, r[nn][j], bad);
-            if (ok[nn][j]) Raw::template clear<RDW>(slot_a(d, me, parity, s), u);
+            uint4* slot = reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(s) * a_stride);
+            ok[nn][j] = Raw::template try_get<RDW>(slot, u, c.seq, r[nn][j], bad);
+            if (ok[nn][j]) Raw::template clear<RDW>(slot, u);
           }
+          l = l + 1 == G ? 0 : l + 1;
         }
       }
     }
@@ -501,11 +520,13 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 #pragma unroll
       for (int j = 0; j < MAXG; ++j) {
         if (j < G && !ok[nn][j]) {
-          const int s = nn * G + (c0 + 1 + j) % G;
-          recv_unit<Raw, RDW>(c, slot_a(d, me, parity, s), u, r[nn][j], s);
+          const int s = src[nn][j];
+          recv_unit<Raw, RDW>(c, reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(s) * a_stride),
+                              u, r[nn][j], s);
         }
       }
     }
+    const int c3 = straddle ? c0 + 1 : c0;
 
     // Node partials, combined on the fly into the pairwise tree over nodes
     // (node order == the XOR-step adds): stack[k] holds a finished subtree of
@@ -529,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         // The unit straddles a shard boundary: per-element fold order.
 #pragma unroll
         for (int q = 0; q < UE; ++q) {
-          const int cq = q < valid ? static_cast<int>((e0 + q) / SG) : c0;
+          const int cq = q < valid ? static_cast<int>((e0 + q) / SG32) : c0;
           const int rot = cq - c0;
           A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % G, q);
 #pragma unroll
@@ -560,22 +581,28 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
     store_raw<E, UE>(recv, e0, valid, o);
     if (!oneshot) {
+      int q = me;
       for (int j = 1; j < P; ++j) {
-        Raw::template put<RDW>(slot_b(d, (me + j) % P, parity, me), u, o, c.seq);
+        q = q + 1 == P ? 0 : q + 1;
+        Raw::template put<RDW>(slot_b(d, q, parity, me), u, o, c.seq);
       }
     }
   }
   stamp(d, 4);
 
   if (!oneshot) {
+    uint8_t* const b_mine = d.base[me] + d.lay.b_off + static_cast<uint64_t>(parity) * d.world * d.lay.b_src * 8;
+    const uint64_t b_stride = d.lay.b_src * 8;
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+      int q = me;
       for (int j = 1; j < P; ++j) {
-        const int q = (me + P - j) % P;
-        const uint64_t e0 = static_cast<uint64_t>(q) * SP + UE * u;
-        const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+        q = q == 0 ? P - 1 : q - 1;
+        const uint32_t e0 = static_cast<uint32_t>(q * SP) + UE * static_cast<uint32_t>(u);
+        const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
         if (valid == 0) continue;
         uint32_t r[RDW];
-        recv_unit<Raw, RDW>(c, slot_b(d, me, parity, q), u, r, q);
+        recv_unit<Raw, RDW>(c, reinterpret_cast<uint4*>(b_mine + static_cast<uint64_t>(q) * b_stride),
+                            u, r, q);
         store_raw<E, UE>(recv, e0, valid, r);
       }
     }
