@@ -197,6 +197,10 @@ int nvrar_set_profile(nvrar_comm_t comm, int on);
 int nvrar_get_phase_times(nvrar_comm_t comm, uint64_t* ts, int n);
 int nvrar_pingpong(nvrar_comm_t comm, int peer, int iters, int initiator, void* stream,
                    uint64_t* elapsed_ns);
+/* Absolute %globaltimer stamps of the last ping-pong round on this rank:
+ * initiator {last send, last receive}; responder {last receive, same}. With both
+ * sides one can estimate the offset between the two GPUs' global timers. */
+int nvrar_pingpong_clock(nvrar_comm_t comm, uint64_t* stamps);
 const char* nvrar_last_error(nvrar_comm_t comm);
 const char* nvrar_status_string(int status);
 int nvrar_abi_version(void);

@@ -103,7 +103,8 @@ SIGNATURES = {
     "nvrar_get_phase_times": (_c.c_int, [_vp, _c.POINTER(_c.c_uint64), _c.c_int]),
     "nvrar_pingpong": (_c.c_int, [_vp, _c.c_int, _c.c_int, _c.c_int, _vp,
                                   _c.POINTER(_c.c_uint64)]),
-    "nvrar_check": (_c.c_int, [_vp]),
+    "nvrar_pingpong_clock": (_c.c_int, [_vp, _c.POINTER(_c.c_uint64)]),
+    "nvrar_check":(_c.c_int, [_vp]),
     "nvrar_get_blocked": (_c.c_int, [_vp, _c.POINTER(Blocked)]),
     "nvrar_last_error": (_c.c_char_p, [_vp]),
     "nvrar_status_string": (_c.c_char_p, [_c.c_int]),

@@ -703,6 +703,13 @@ int nvrar_pingpong(nvrar_comm_t c, int peer, int iters, int initiator, void* str
   return NVRAR_SUCCESS;
 }
 
+int nvrar_pingpong_clock(nvrar_comm_t c, uint64_t* stamps) {
+  if (!c || !stamps) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpy(stamps, c->d_scratch + 1, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_get_blocked(nvrar_comm_t c, nvrar_blocked_t* out) {
   if (!c || !out) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
   CUDA_TRY(c, cudaSetDevice(c->device));

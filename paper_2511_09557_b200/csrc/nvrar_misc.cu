@@ -25,18 +25,28 @@ __global__ void pingpong_kernel(const __grid_constant__ LaunchParams lp, int pee
   uint64_t* theirs = diag_word(d, peer);
   const uint64_t t_limit = globaltimer() + d.timeout_ns;
   const uint64_t t0 = globaltimer();
+  uint64_t t_last_send = 0, t_last_recv = 0;
   for (int i = 1; i <= iters; ++i) {
     const uint64_t v = base + static_cast<uint64_t>(i);
-    if (initiator) st_volatile64(theirs, v);
+    if (initiator) {
+      t_last_send = globaltimer();
+      st_volatile64(theirs, v);
+    }
     while (ld_volatile64(mine) != v) {
       if (globaltimer() > t_limit) {
         *out_ns = ~0ull;
         return;
       }
     }
+    t_last_recv = globaltimer();
     if (!initiator) st_volatile64(theirs, v);
   }
-  *out_ns = globaltimer() - t0;
+  // [0] initiator's elapsed ns; [1] last send (initiator) / last echo time
+  // (responder); [2] last receive — absolute %globaltimer values, which let the
+  // host estimate the clock offset between the two GPUs.
+  out_ns[0] = globaltimer() - t0;
+  out_ns[1] = initiator ? t_last_send : t_last_recv;
+  out_ns[2] = t_last_recv;
 }
 
 KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu, bool lamport) {
