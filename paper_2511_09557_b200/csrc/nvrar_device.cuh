@@ -328,6 +328,83 @@ __device__ __forceinline__ void recv_unit(Ctl& c, uint4* slot, uint64_t u, uint3
   Pr::template clear<W>(slot, u);
 }
 
+// Receive K cells at once: every round issues one load per still-pending cell
+// (bit k of `pending`), so detection costs one L2 round trip after the LAST
+// arrival instead of one round trip per source. Arrived cells are re-emptied.
+template <class Pr, int W, int K>
+__device__ __forceinline__ void recv_all(Ctl& c, uint4* const (&slot)[K], const uint64_t (&u)[K],
+                                         uint32_t (&d)[K][W], uint32_t pending,
+                                         const int (&peer)[K]) {
+  while (pending) {
+    uint32_t bad = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if ((pending >> k) & 1u) {
+        if (Pr::template try_get<W>(slot[k], u[k], c.seq, d[k], bad)) {
+          Pr::template clear<W>(slot[k], u[k]);
+          pending &= ~(1u << k);
+        } else if (!Pr::kLamport && flag_ahead(bad, c.seq)) {
+          record_fault(c, kProtocolFault, kStaleFlag, peer[k], u[k], bad);
+          return;
+        }
+      }
+    }
+    if (pending) {
+      const int k0 = __ffs(pending) - 1;
+      int pk = peer[0];
+      uint64_t uk = u[0];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (k == k0) {
+          pk = peer[k];
+          uk = u[k];
+        }
+      }
+      if (wait_tick(c, kFlagWait, pk, uk, bad)) return;
+      if (c.poll_ns) __nanosleep(c.poll_ns);
+    }
+  }
+}
+
+// Same, for an [NN][MM] grid of source cells of one unit u (bit nn*MM + m).
+template <class Pr, int W, int NN, int MM>
+__device__ __forceinline__ void recv_grid(Ctl& c, uint4* const (&slot)[NN][MM], uint64_t u,
+                                          uint32_t (&d)[NN][MM][W], uint32_t pending,
+                                          const int (&peer)[NN][MM]) {
+  while (pending) {
+    uint32_t bad = 0;
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const uint32_t bit = 1u << (a * MM + m);
+        if (pending & bit) {
+          if (Pr::template try_get<W>(slot[a][m], u, c.seq, d[a][m], bad)) {
+            Pr::template clear<W>(slot[a][m], u);
+            pending &= ~bit;
+          } else if (!Pr::kLamport && flag_ahead(bad, c.seq)) {
+            record_fault(c, kProtocolFault, kStaleFlag, peer[a][m], u, bad);
+            return;
+          }
+        }
+      }
+    }
+    if (pending) {
+      const int k0 = __ffs(pending) - 1;
+      int pk = 0;
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+          if (a * MM + m == k0) pk = peer[a][m];
+        }
+      }
+      if (wait_tick(c, kFlagWait, pk, u, bad)) return;
+      if (c.poll_ns) __nanosleep(c.poll_ns);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Element traits. RAW is the caller dtype's bits, ACC the arithmetic type
 // (fp32 for float/bf16, wrapping uint32 for int32).

@@ -255,31 +255,24 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
         raw_to_acc<UE>(E{}, own, f[k]);
         continue;
       }
-      uint32_t r[kHierMaxG - 1][RDW];
-      bool ok[kHierMaxG - 1];
-      uint32_t bad = 0;
+      uint32_t r[1][kHierMaxG - 1][RDW];
+      uint4* slots[1][kHierMaxG - 1];
+      int peers[1][kHierMaxG - 1];
+      uint32_t pending = 0;
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
-        if (j < G) {
-          ok[j - 1] = Raw::template try_get<RDW>(slot_a(d, me, parity, grp[j]), uu[k],
-                                                 c.seq, r[j - 1], bad);
-          if (ok[j - 1]) Raw::template clear<RDW>(slot_a(d, me, parity, grp[j]), uu[k]);
-        }
+        slots[0][j - 1] = slot_a(d, me, parity, grp[j]);
+        peers[0][j - 1] = node * G + grp[j];
+        if (j < G) pending |= 1u << (j - 1);
       }
-#pragma unroll
-      for (int j = 1; j < kHierMaxG; ++j) {
-        if (j < G && !ok[j - 1]) {
-          const int s = grp[j];
-          recv_unit<Raw, RDW>(c, slot_a(d, me, parity, s), uu[k], r[j - 1], node * G + s);
-        }
-      }
+      recv_grid<Raw, RDW, 1, kHierMaxG - 1>(c, slots, uu[k], r, pending, peers);
       // c owns in[c] + (in[c-1] + (... + (in[c+2] + in[c+1])))  (ring_schedule.hpp:12-15)
-      raw_to_acc<UE>(E{}, r[0], f[k]);
+      raw_to_acc<UE>(E{}, r[0][0], f[k]);
 #pragma unroll
       for (int j = 2; j < kHierMaxG; ++j) {
         if (j < G) {
           A a[UE];
-          raw_to_acc<UE>(E{}, r[j - 1], a);
+          raw_to_acc<UE>(E{}, r[0][j - 1], a);
 #pragma unroll
           for (int q = 0; q < UE; ++q) f[k][q] = acc_add(f[k][q], a[q]);
         }
@@ -303,13 +296,22 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
         Part::template put<UE>(dst, uu[k], b, c.seq);
       }
       uint4* src = slot_c(d, me, parity, l);
+      uint4* srcs[kHierUpt];
+      int partners[kHierUpt];
+      uint32_t b[kHierUpt][UE];
+      uint32_t pending = 0;
+#pragma unroll
+      for (int k = 0; k < kHierUpt; ++k) {
+        srcs[k] = src;
+        partners[k] = partner;
+        if (valid[k] > 0) pending |= 1u << k;
+      }
+      recv_all<Part, UE, kHierUpt>(c, srcs, uu, b, pending, partners);
 #pragma unroll
       for (int k = 0; k < kHierUpt; ++k) {
         if (valid[k] == 0) continue;
-        uint32_t b[UE];
-        recv_unit<Part, UE>(c, src, uu[k], b, partner);
         A p[UE];
-        bits_acc<UE>(b, p);
+        bits_acc<UE>(b[k], p);
 #pragma unroll
         for (int q = 0; q < UE; ++q) f[k][q] = acc_add(p[q], f[k][q]);
       }
@@ -335,30 +337,27 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   // Phase 3b: all-gather receive.
   if (G > 1) {
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-      uint32_t r[kHierMaxG - 1][RDW];
-      bool ok[kHierMaxG - 1];
+      uint32_t r[1][kHierMaxG - 1][RDW];
+      uint4* slots[1][kHierMaxG - 1];
+      int peers[1][kHierMaxG - 1];
       int valid[kHierMaxG - 1];
-      uint32_t bad = 0;
+      uint32_t pending = 0;
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
+        const int s = grp[j];
+        slots[0][j - 1] = slot_b(d, me, parity, s);
+        peers[0][j - 1] = node * G + s;
+        valid[j - 1] = 0;
         if (j < G) {
-          const int s = grp[j];
           valid[j - 1] = chunk_valid<UE>(S, u, n, static_cast<uint64_t>(s) * S);
-          ok[j - 1] = valid[j - 1] == 0;
-          if (!ok[j - 1]) {
-            ok[j - 1] = Raw::template try_get<RDW>(slot_b(d, me, parity, s), u, c.seq, r[j - 1], bad);
-            if (ok[j - 1]) Raw::template clear<RDW>(slot_b(d, me, parity, s), u);
-          }
+          if (valid[j - 1] > 0) pending |= 1u << (j - 1);
         }
       }
+      recv_grid<Raw, RDW, 1, kHierMaxG - 1>(c, slots, u, r, pending, peers);
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
-        if (j < G) {
-          const int s = grp[j];
-          if (!ok[j - 1]) recv_unit<Raw, RDW>(c, slot_b(d, me, parity, s), u, r[j - 1], node * G + s);
-          if (valid[j - 1] > 0) {
-            store_raw<E, UE>(recv, static_cast<uint64_t>(s) * S + UE * u, valid[j - 1], r[j - 1]);
-          }
+        if (j < G && valid[j - 1] > 0) {
+          store_raw<E, UE>(recv, static_cast<uint64_t>(grp[j]) * S + UE * u, valid[j - 1], r[0][j - 1]);
         }
       }
     }
@@ -489,16 +488,16 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     // Every source's unit, in fold order relative to c0: r[nn][j] is the copy
     // of local rank (c0+1+j) % G of node nn.
     uint32_t r[N][MAXG][RDW];
-    bool ok[N][MAXG];
+    uint4* slots[N][MAXG];
     int src[N][MAXG];
-    uint32_t bad = 0;
+    uint32_t pending = 0;
 #pragma unroll
     for (int nn = 0; nn < N; ++nn) {
       int l = l0;
 #pragma unroll
       for (int j = 0; j < MAXG; ++j) {
-        ok[nn][j] = true;
         src[nn][j] = nn * G + l;
+        slots[nn][j] = reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(src[nn][j]) * a_stride);
         if (j < G) {
           const int s = src[nn][j];
           if (s == me && u == u_first) {
@@ -507,25 +506,13 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
           } else if (s == me) {
             load_raw<E, UE>(send, e0, valid, r[nn][j]);
           } else {
-            uint4* slot = reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(s) * a_stride);
-            ok[nn][j] = Raw::template try_get<RDW>(slot, u, c.seq, r[nn][j], bad);
-            if (ok[nn][j]) Raw::template clear<RDW>(slot, u);
+            pending |= 1u << (nn * MAXG + j);
           }
           l = l + 1 == G ? 0 : l + 1;
         }
       }
     }
-#pragma unroll
-    for (int nn = 0; nn < N; ++nn) {
-#pragma unroll
-      for (int j = 0; j < MAXG; ++j) {
-        if (j < G && !ok[nn][j]) {
-          const int s = src[nn][j];
-          recv_unit<Raw, RDW>(c, reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(s) * a_stride),
-                              u, r[nn][j], s);
-        }
-      }
-    }
+    recv_grid<Raw, RDW, N, MAXG>(c, slots, u, r, pending, src);
     const int c3 = straddle ? c0 + 1 : c0;
 
     // Node partials, combined on the fly into the pairwise tree over nodes
@@ -593,17 +580,37 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   if (!oneshot) {
     uint8_t* const b_mine = d.base[me] + d.lay.b_off + static_cast<uint64_t>(parity) * d.world * d.lay.b_src * 8;
     const uint64_t b_stride = d.lay.b_src * 8;
+    constexpr int kGrp = 8;  // sources polled together (P <= 8: one group)
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
       int q = me;
-      for (int j = 1; j < P; ++j) {
-        q = q == 0 ? P - 1 : q - 1;
-        const uint32_t e0 = static_cast<uint32_t>(q * SP) + UE * static_cast<uint32_t>(u);
-        const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
-        if (valid == 0) continue;
-        uint32_t r[RDW];
-        recv_unit<Raw, RDW>(c, reinterpret_cast<uint4*>(b_mine + static_cast<uint64_t>(q) * b_stride),
-                            u, r, q);
-        store_raw<E, UE>(recv, e0, valid, r);
+      for (int j0 = 1; j0 < P; j0 += kGrp) {
+        uint32_t r[1][kGrp][RDW];
+        uint4* slots[1][kGrp];
+        int qs[1][kGrp];
+        int valid[kGrp];
+        uint32_t pending = 0;
+#pragma unroll
+        for (int t = 0; t < kGrp; ++t) {
+          valid[t] = 0;
+          qs[0][t] = q;
+          slots[0][t] = reinterpret_cast<uint4*>(b_mine);
+          if (j0 + t < P) {
+            q = q == 0 ? P - 1 : q - 1;
+            qs[0][t] = q;
+            slots[0][t] = reinterpret_cast<uint4*>(b_mine + static_cast<uint64_t>(q) * b_stride);
+            const uint32_t e0 = static_cast<uint32_t>(q * SP) + UE * static_cast<uint32_t>(u);
+            valid[t] = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
+            if (valid[t] > 0) pending |= 1u << t;
+          }
+        }
+        recv_grid<Raw, RDW, 1, kGrp>(c, slots, u, r, pending, qs);
+#pragma unroll
+        for (int t = 0; t < kGrp; ++t) {
+          if (valid[t] > 0) {
+            store_raw<E, UE>(recv, static_cast<uint32_t>(qs[0][t] * SP) + UE * static_cast<uint32_t>(u),
+                             valid[t], r[0][t]);
+          }
+        }
       }
     }
   }
