@@ -1,0 +1,69 @@
+"""Single-GPU twin of tests/mp_stress.py: the same deterministic sequence of
+calls (switching schedule, CTA count, dtype, size) on virtual ranks of one GPU,
+each checked against an exactly representable expected sum.
+
+    python tests/stress_emu.py --calls 3000 --nodes 2 --gpus 2
+"""
+import argparse
+import os
+import random
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2511_09557_b200 import ClusterTopology, LocalGroup, NvrarConfig  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--calls", type=int, default=2000)
+    ap.add_argument("--nodes", type=int, default=2)
+    ap.add_argument("--gpus", type=int, default=2)
+    ap.add_argument("--timeout", type=float, default=3.0)
+    ap.add_argument("--start", type=int, default=0, help="first call to run (skip earlier ones)")
+    ap.add_argument("--verbose", action="store_true")
+    args = ap.parse_args()
+    world = args.nodes * args.gpus
+    g = LocalGroup(ClusterTopology(args.nodes, args.gpus), 4 << 20, device=0,
+                   timeout_s=args.timeout)
+    rng = random.Random(1234)
+    sizes = [1, 7, 1000, 4099, 65536, 131072, 300001, 1 << 20]
+    algos = ["hier", "twoshot", "oneshot", "auto"]
+    dtypes = [torch.bfloat16, torch.float32, torch.int32]
+    total = world * (world + 1) // 2
+    for it in range(args.calls):
+        algo = rng.choice(algos)
+        blocks = rng.choice([0, 1, 3, 16, 32, 128])
+        dt = rng.choice(dtypes)
+        n = rng.choice(sizes)
+        if dt != torch.int32 and n > (1 << 20) // 2:
+            n = (1 << 20) // 2
+        if it < args.start:
+            continue
+        g.set_algo(algo)
+        g.set_config(NvrarConfig(blocks, 65536))
+        idx = torch.arange(n, device="cuda", dtype=torch.int64) % 7 + 1
+        xs = [(idx * (r + 1)).to(dt) for r in range(world)]
+        ys = [torch.empty_like(x) for x in xs]
+        if args.verbose:
+            print(it, algo, blocks, dt, n, g.comms[0].plan(n, dt), flush=True)
+        try:
+            g.run_all(xs, ys)
+        except Exception as e:  # noqa: BLE001
+            print(f"call {it} ({algo}/{blocks} {dt} n={n} plan={g.comms[0].plan(n, dt)}): {e}")
+            return 1
+        want = (idx * total).to(dt)
+        for r, y in enumerate(ys):
+            if not torch.equal(y, want):
+                print(f"call {it} ({algo}/{blocks} {dt} n={n}): rank {r} "
+                      f"{int((y != want).sum())} wrong")
+                return 1
+    print(f"OK after {args.calls} calls")
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
