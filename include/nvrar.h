@@ -201,6 +201,10 @@ int nvrar_pingpong(nvrar_comm_t comm, int peer, int iters, int initiator, void* 
  * initiator {last send, last receive}; responder {last receive, same}. With both
  * sides one can estimate the offset between the two GPUs' global timers. */
 int nvrar_pingpong_clock(nvrar_comm_t comm, uint64_t* stamps);
+/* Invariant check (tests): count the 8-byte words of the slot areas that are
+ * not empty (all ones) — between calls every slot must be empty. Synchronises.
+ * `first_offset` receives the byte offset of the first dirty word (or ~0). */
+int nvrar_debug_dirty_cells(nvrar_comm_t comm, uint64_t* dirty, uint64_t* first_offset);
 const char* nvrar_last_error(nvrar_comm_t comm);
 const char* nvrar_status_string(int status);
 int nvrar_abi_version(void);

@@ -288,6 +288,12 @@ class Communicator:
     def last_error(self) -> str:
         return self._lib.nvrar_last_error(self._h).decode()
 
+    def dirty_cells(self):
+        """(count, first byte offset) of non-empty slot words — must be (0, -1) between calls."""
+        cnt, first = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(self._lib.nvrar_debug_dirty_cells(self._h, ctypes.byref(cnt), ctypes.byref(first)))
+        return cnt.value, (-1 if first.value == (1 << 64) - 1 else first.value)
+
     def symmetric_bytes(self) -> int:
         return int(self._lib.nvrar_symmetric_bytes(self._h))
 

@@ -703,6 +703,24 @@ int nvrar_pingpong(nvrar_comm_t c, int peer, int iters, int initiator, void* str
   return NVRAR_SUCCESS;
 }
 
+int nvrar_debug_dirty_cells(nvrar_comm_t c, uint64_t* dirty, uint64_t* first_offset) {
+  if (!c || !dirty) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  std::vector<uint64_t> h((c->lay.bytes - c->lay.a_off) / 8);
+  CUDA_TRY(c, cudaMemcpy(h.data(), c->region + c->lay.a_off, h.size() * 8, cudaMemcpyDeviceToHost));
+  uint64_t cnt = 0, first = ~0ull;
+  for (size_t i = 0; i < h.size(); ++i) {
+    if (h[i] != ~0ull) {
+      if (first == ~0ull) first = c->lay.a_off + i * 8;
+      ++cnt;
+    }
+  }
+  *dirty = cnt;
+  if (first_offset) *first_offset = first;
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_pingpong_clock(nvrar_comm_t c, uint64_t* stamps) {
   if (!c || !stamps) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
   CUDA_TRY(c, cudaSetDevice(c->device));

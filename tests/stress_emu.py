@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--timeout", type=float, default=3.0)
     ap.add_argument("--start", type=int, default=0, help="first call to run (skip earlier ones)")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--check-dirty", action="store_true",
+                    help="after every call, every slot word must be empty (all ones)")
     args = ap.parse_args()
     world = args.nodes * args.gpus
     g = LocalGroup(ClusterTopology(args.nodes, args.gpus), 4 << 20, device=0,
@@ -61,6 +63,13 @@ def main():
                 print(f"call {it} ({algo}/{blocks} {dt} n={n}): rank {r} "
                       f"{int((y != want).sum())} wrong")
                 return 1
+        if args.check_dirty:
+            for r, c in enumerate(g.comms):
+                cnt, first = c.dirty_cells()
+                if cnt:
+                    print(f"call {it} ({algo}/{blocks} {dt} n={n} plan={g.comms[0].plan(n, dt)}): "
+                          f"rank {r} left {cnt} non-empty slot words (first at byte {first})")
+                    return 1
     print(f"OK after {args.calls} calls")
     return 0
 
