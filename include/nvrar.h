@@ -138,6 +138,8 @@ typedef struct {
   uint64_t word_index;
   uint64_t observed;
   int status;         /* nvrar_status_t of the fault */
+  int phase;          /* kernel phase: 2 push, 3 peer sync, 4 reduce/RD, 5 all-gather */
+  int cta;            /* CTA index that recorded the wait */
 } nvrar_blocked_t;
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -71,6 +71,8 @@ class Blocked(ctypes.Structure):
         ("word_index", ctypes.c_uint64),
         ("observed", ctypes.c_uint64),
         ("status", ctypes.c_int),
+        ("phase", ctypes.c_int),
+        ("cta", ctypes.c_int),
     ]
 
 

@@ -62,6 +62,8 @@ class BlockedRank:
     word_index: int = 0
     peer_rank: int = -1
     expected: int = 0
+    phase: int = -1  # GPU diagnosis: kernel phase (2 push, 3 sync, 4 reduce/RD, 5 all-gather)
+    cta: int = -1
 
 
 class DeadlockError(RuntimeError):
@@ -73,7 +75,7 @@ class DeadlockError(RuntimeError):
         for b in self._blocked:
             if b.kind == BlockedRank.Kind.FlagWait:
                 parts.append(f"[rank {b.global_rank} awaits flag {b.expected} from rank "
-                             f"{b.peer_rank} word {b.word_index}]")
+                             f"{b.peer_rank} word {b.word_index} (phase {b.phase}, cta {b.cta})]")
             else:
                 parts.append(f"[rank {b.global_rank} awaits seq {b.expected} from rank "
                              f"{b.peer_rank}]")
@@ -333,7 +335,8 @@ class Communicator:
 def _blocked_rank(b: L.Blocked) -> BlockedRank:
     return BlockedRank(global_rank=b.global_rank,
                        kind=BlockedRank.Kind.SeqWait if b.kind == 1 else BlockedRank.Kind.FlagWait,
-                       word_index=b.word_index, peer_rank=b.peer_rank, expected=b.expected)
+                       word_index=b.word_index, peer_rank=b.peer_rank, expected=b.expected,
+                       phase=b.phase, cta=b.cta)
 
 
 def _check_pair(send: torch.Tensor, recv: torch.Tensor) -> None:

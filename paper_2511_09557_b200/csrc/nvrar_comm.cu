@@ -741,6 +741,8 @@ int nvrar_get_blocked(nvrar_comm_t c, nvrar_blocked_t* out) {
   out->word_index = st.err.word;
   out->observed = st.err.observed;
   out->status = static_cast<int>(st.err.code);
+  out->phase = st.err.phase;
+  out->cta = st.err.cta;
   return NVRAR_SUCCESS;
 }
 

@@ -61,6 +61,8 @@ struct ErrRec {
   uint32_t expected;  // awaited sequence number
   uint64_t word;      // unit index inside the awaited slot (FlagWait)
   uint64_t observed;  // what was seen instead
+  int32_t phase;      // kernel phase of the wait (2 RS/push, 3 sync, 4 reduce/RD, 5 AG)
+  int32_t cta;        // CTA that recorded it
 };
 
 // Private (not shared) per-rank state. seq is the NvrarAllreduce::seq_ analogue
@@ -160,6 +162,7 @@ struct Ctl {
   uint32_t spins;
   uint64_t t0;
   bool aborted;
+  int phase;
 };
 
 __device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, int peer,
@@ -171,6 +174,8 @@ __device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, in
     e->expected = c.seq;
     e->word = word;
     e->observed = observed;
+    e->phase = c.phase;
+    e->cta = static_cast<int32_t>(blockIdx.x);
     __threadfence();
     atomicExch(&e->code, code);
   }

@@ -92,6 +92,7 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
   c.aborted = false;
   c.t0 = globaltimer();
   c.seq = s_seq + 1u;
+  c.phase = 2;
   stamp(d, 1);
   return s_err == 0u;
 }
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
   }
   stamp(d, 2);
+  c.phase = 3;
 
   // Peer-only sync, wait half: all log2(N) XOR peers before any RD send.
   if (kSteps > 0) {
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     __syncthreads();
   }
   stamp(d, 3);
+  c.phase = 4;
 
   // Phases 1b+2+3a: fold own chunk, recursive doubling, cast + all-gather push.
   const uint64_t mybase = static_cast<uint64_t>(local) * S;
@@ -333,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
   }
   stamp(d, 4);
+  c.phase = 5;
 
   // Phase 3b: all-gather receive.
   if (G > 1) {
@@ -462,12 +466,14 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
   }
   stamp(d, 2);
+  c.phase = 3;
 
   for (int p = threadIdx.x; p < P; p += blockDim.x) {
     if (p != me) wait_seq_len(c, d, p, n);
   }
   __syncthreads();
   stamp(d, 3);
+  c.phase = 4;
 
   // Index math in 32 bits (counts < 2^31 elements) and slot bases hoisted out
   // of the unit loop: per unit the kernel does one division (the shard of the
@@ -576,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
   }
   stamp(d, 4);
+  c.phase = 5;
 
   if (!oneshot) {
     uint8_t* const b_mine = d.base[me] + d.lay.b_off + static_cast<uint64_t>(parity) * d.world * d.lay.b_src * 8;
