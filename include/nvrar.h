@@ -207,6 +207,11 @@ int nvrar_pingpong_clock(nvrar_comm_t comm, uint64_t* stamps);
  * not empty (all ones) — between calls every slot must be empty. Synchronises.
  * `first_offset` receives the byte offset of the first dirty word (or ~0). */
 int nvrar_debug_dirty_cells(nvrar_comm_t comm, uint64_t* dirty, uint64_t* first_offset);
+/* Debug: copy `bytes` of this rank's symmetric region at `offset` to host;
+ * `layout` (if non-null) receives the 8 layout words (ctrl, a_off, a_src, b_off,
+ * b_src, c_off, c_step, bytes). Synchronises. */
+int nvrar_debug_read_region(nvrar_comm_t comm, uint64_t offset, uint64_t bytes, void* host,
+                            uint64_t* layout);
 const char* nvrar_last_error(nvrar_comm_t comm);
 const char* nvrar_status_string(int status);
 int nvrar_abi_version(void);

@@ -721,6 +721,22 @@ int nvrar_debug_dirty_cells(nvrar_comm_t c, uint64_t* dirty, uint64_t* first_off
   return NVRAR_SUCCESS;
 }
 
+int nvrar_debug_read_region(nvrar_comm_t c, uint64_t offset, uint64_t bytes, void* host,
+                            uint64_t* layout) {
+  if (!c || (!host && bytes)) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  if (layout) {
+    const uint64_t l[8] = {c->lay.ctrl_off, c->lay.a_off, c->lay.a_src, c->lay.b_off,
+                           c->lay.b_src, c->lay.c_off, c->lay.c_step, c->lay.bytes};
+    std::memcpy(layout, l, sizeof(l));
+  }
+  if (!bytes) return NVRAR_SUCCESS;
+  if (offset + bytes > c->lay.bytes) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "out of range");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  CUDA_TRY(c, cudaMemcpy(host, c->region + offset, bytes, cudaMemcpyDeviceToHost));
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_pingpong_clock(nvrar_comm_t c, uint64_t* stamps) {
   if (!c || !stamps) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
   CUDA_TRY(c, cudaSetDevice(c->device));

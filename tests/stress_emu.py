@@ -17,6 +17,27 @@ sys.path.insert(0, ROOT)
 from paper_2511_09557_b200 import ClusterTopology, LocalGroup, NvrarConfig  # noqa: E402
 
 
+def dump_cell(g, b, args, world, n, ys, dt):
+    """Print the awaited all-gather cell (hier, Lamport, 1 cell/unit) and the peer's output."""
+    import ctypes
+    c = g.comms[b.global_rank]
+    lay = (ctypes.c_uint64 * 8)()
+    c._lib.nvrar_debug_read_region(c._h, 0, 0, None, lay)
+    parity = b.expected & 1
+    src_local = b.peer_rank % args.gpus
+    area = {5: (lay[3], lay[4]), 4: (lay[1], lay[2])}.get(b.phase, (lay[3], lay[4]))
+    off = area[0] + (parity * world + src_local) * area[1] * 8 + b.word_index * 16
+    buf = (ctypes.c_uint32 * 16)()
+    c._lib.nvrar_debug_read_region(c._h, off - 16, 64, buf, None)
+    print(f"  rank {b.global_rank} phase {b.phase} cta {b.cta}: cells around unit {b.word_index}: "
+          + " ".join(f"{v:08x}" for v in buf))
+    S = (n + args.gpus - 1) // args.gpus
+    peer_chunk = b.peer_rank % args.gpus
+    lo = peer_chunk * S + 8 * b.word_index
+    print(f"  peer {b.peer_rank} output[{lo}:{lo + 8}] = {ys[b.peer_rank][lo:lo + 8].tolist()}; "
+          f"receiver output = {ys[b.global_rank][lo:lo + 8].tolist()}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--calls", type=int, default=2000)
@@ -56,6 +77,8 @@ def main():
             g.run_all(xs, ys)
         except Exception as e:  # noqa: BLE001
             print(f"call {it} ({algo}/{blocks} {dt} n={n} plan={g.comms[0].plan(n, dt)}): {e}")
+            for b in getattr(e, "blocked", lambda: [])():
+                dump_cell(g, b, args, world, n, ys, dt)
             return 1
         want = (idx * total).to(dt)
         for r, y in enumerate(ys):
