@@ -212,6 +212,8 @@ int nvrar_debug_dirty_cells(nvrar_comm_t comm, uint64_t* dirty, uint64_t* first_
  * b_src, c_off, c_step, bytes). Synchronises. */
 int nvrar_debug_read_region(nvrar_comm_t comm, uint64_t offset, uint64_t bytes, void* host,
                             uint64_t* layout);
+/* Debug: the per-CTA replicas of the call counter (all equal between calls). */
+int nvrar_debug_seq_slots(nvrar_comm_t comm, uint32_t* out, int n);
 const char* nvrar_last_error(nvrar_comm_t comm);
 const char* nvrar_status_string(int status);
 int nvrar_abi_version(void);

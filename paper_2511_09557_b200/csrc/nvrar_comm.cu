@@ -737,6 +737,15 @@ int nvrar_debug_read_region(nvrar_comm_t c, uint64_t offset, uint64_t bytes, voi
   return NVRAR_SUCCESS;
 }
 
+int nvrar_debug_seq_slots(nvrar_comm_t c, uint32_t* out, int n) {
+  if (!c || !out || n < 1) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  CUDA_TRY(c, cudaMemcpy(out, c->state->seq, sizeof(uint32_t) * std::min(n, kSeqSlots),
+                         cudaMemcpyDeviceToHost));
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_pingpong_clock(nvrar_comm_t c, uint64_t* stamps) {
   if (!c || !stamps) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
   CUDA_TRY(c, cudaSetDevice(c->device));

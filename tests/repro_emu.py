@@ -45,6 +45,14 @@ def main():
             g.check()
         except Exception as e:  # noqa: BLE001
             print(f"after <= {done} calls: {e}")
+            import ctypes
+            from collections import Counter
+            for r, c in enumerate(g.comms):
+                s = (ctypes.c_uint32 * 512)()
+                c._lib.nvrar_debug_seq_slots(c._h, s, 512)
+                cnt = Counter(list(s))
+                odd = [i for i in range(512) if s[i] != cnt.most_common(1)[0][0]]
+                print(f"  rank {r} seq slots {dict(cnt)} odd slots {odd[:20]}")
             return 1
         for r in range(world):
             if not torch.equal(ys[r], want):
