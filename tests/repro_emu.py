@@ -53,6 +53,27 @@ def main():
                 cnt = Counter(list(s))
                 odd = [i for i in range(512) if s[i] != cnt.most_common(1)[0][0]]
                 print(f"  rank {r} seq slots {dict(cnt)} odd slots {odd[:20]}")
+            for b in getattr(e, "blocked", lambda: [])():
+                c = g.comms[b.global_rank]
+                lay = (ctypes.c_uint64 * 8)()
+                c._lib.nvrar_debug_read_region(c._h, 0, 0, None, lay)
+                parity = b.expected & 1
+                src = b.peer_rank % args.gpus
+                base = {5: (lay[3], lay[4]), 4: (lay[1], lay[2])}.get(b.phase, (lay[3], lay[4]))
+                off = base[0] + (parity * world + src) * base[1] * 8 + b.word_index * 16
+                buf = (ctypes.c_uint32 * 16)()
+                c._lib.nvrar_debug_read_region(c._h, off - 16, 64, buf, None)
+                print(f"  rank {b.global_rank} cells [u-1..u+2] of src {src} parity {parity}: "
+                      + " ".join(f"{v:08x}" for v in buf))
+                other = (ctypes.c_uint32 * 16)()
+                off2 = base[0] + ((1 - parity) * world + src) * base[1] * 8 + b.word_index * 16
+                c._lib.nvrar_debug_read_region(c._h, off2 - 16, 64, other, None)
+                print(f"  same cells, other parity: " + " ".join(f"{v:08x}" for v in other))
+                cnt2 = ctypes.c_uint64()
+                first = ctypes.c_uint64()
+                c._lib.nvrar_debug_dirty_cells(c._h, ctypes.byref(cnt2), ctypes.byref(first))
+                print(f"  rank {b.global_rank} dirty words {cnt2.value} first at {first.value} "
+                      f"(awaited cell at {off})")
             return 1
         for r in range(world):
             if not torch.equal(ys[r], want):
