@@ -119,9 +119,12 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // stores is what keeps several HBM loads in flight per thread. (asm volatile
 // statements still keep their order among themselves: read-then-empty of a
 // cell stays in program order. pdl_wait keeps its clobber.)
+#ifndef NVRAR_POLL_LD
+#define NVRAR_POLL_LD "ld.volatile.global.v4.u32"
+#endif
 __device__ __forceinline__ uint4 ld_volatile16(const void* p) {
   uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile(NVRAR_POLL_LD " {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
