@@ -166,6 +166,7 @@ struct Ctl {
   uint64_t t0;
   bool aborted;
   int phase;
+  bool last_chance;
 };
 
 __device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, int peer,
@@ -196,10 +197,25 @@ __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t w
   }
   const uint64_t now = globaltimer();
   if (now - c.t0 > c.timeout_ns) {
+    // A thread can be descheduled between its poll and this check; declare a
+    // deadlock only if the wait is still unsatisfied after one more full round.
+    if (!c.last_chance) {
+      c.last_chance = true;
+      c.spins |= 127u;
+      return false;
+    }
     record_fault(c, kDeadlock, kind, peer, word, observed);
     return true;
   }
   return false;
+}
+
+// Back-off between unsatisfied polling rounds. It is also the yield point that
+// lets the other diverged lane groups of the warp run: a tight spin without it
+// was observed to starve lanes whose data had already arrived (independent
+// thread scheduling does not rotate diverged groups often enough).
+__device__ __forceinline__ void poll_pause(const Ctl& c) {
+  __nanosleep(c.poll_ns ? c.poll_ns : 32u);
 }
 
 // flag observed in a slot for call `seq`: equal = arrived; behind = not yet
@@ -331,7 +347,7 @@ __device__ __forceinline__ void recv_unit(Ctl& c, uint4* slot, uint64_t u, uint3
       return;
     }
     if (wait_tick(c, kFlagWait, peer, u, bad)) return;
-    if (c.poll_ns) __nanosleep(c.poll_ns);
+    poll_pause(c);
   }
   Pr::template clear<W>(slot, u);
 }
@@ -369,7 +385,7 @@ __device__ __forceinline__ void recv_all(Ctl& c, uint4* const (&slot)[K], const 
         }
       }
       if (wait_tick(c, kFlagWait, pk, uk, bad)) return;
-      if (c.poll_ns) __nanosleep(c.poll_ns);
+      poll_pause(c);
     }
   }
 }
@@ -408,7 +424,7 @@ __device__ __forceinline__ void recv_grid(Ctl& c, uint4* const (&slot)[NN][MM], 
         }
       }
       if (wait_tick(c, kFlagWait, pk, u, bad)) return;
-      if (c.poll_ns) __nanosleep(c.poll_ns);
+      poll_pause(c);
     }
   }
 }

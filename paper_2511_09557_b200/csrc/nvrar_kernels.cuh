@@ -90,6 +90,7 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
   c.poll_ns = d.poll_ns;
   c.spins = 0;
   c.aborted = false;
+  c.last_chance = false;
   c.t0 = globaltimer();
   c.seq = s_seq + 1u;
   c.phase = 2;
@@ -125,6 +126,7 @@ __device__ __forceinline__ void wait_seq_len(Ctl& c, const RankDesc& d, int peer
     }
     if (flag_ahead(s, c.seq)) return;
     if (wait_tick(c, kSeqWait, peer, 0, v)) return;
+    poll_pause(c);
   }
 }
 
