@@ -130,10 +130,12 @@ __device__ __forceinline__ uint4 ld_volatile16(const void* p) {
   return v;
 }
 
+#ifndef NVRAR_PUT_ST
+#define NVRAR_PUT_ST "st.volatile.global.v4.u32"
+#endif
 __device__ __forceinline__ void st_volatile16(void* p, uint32_t a, uint32_t b, uint32_t c,
                                               uint32_t d) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b),
-               "r"(c), "r"(d));
+  asm volatile(NVRAR_PUT_ST " [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d));
 }
 
 __device__ __forceinline__ uint64_t ld_volatile64(const void* p) {
