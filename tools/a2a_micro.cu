@@ -1,0 +1,165 @@
+// One-shot exchange floor on P GPUs (one process, peer access): every GPU
+// pushes `bytes` of Lamport cells to each of the P-1 others (slot per source)
+// and polls its P-1 incoming slots — the communication of a one-shot
+// all-reduce with nothing else. Stamps %globaltimer; reports the time from the
+// earliest send start to the last arrival over all GPUs (timer offsets from a
+// ping-pong with GPU0).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/a2a_micro tools/a2a_micro.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e = (x);                                                        \
+    if (e != cudaSuccess) {                                                     \
+      printf("%s:%d %s -> %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); \
+      return 1;                                                                 \
+    }                                                                           \
+  } while (0)
+
+constexpr int kMaxP = 8;
+
+struct Peers {
+  uint4* slot[kMaxP];  // slot[p] = my slot inside GPU p's buffer (for my pushes)
+  uint4* in[kMaxP];    // my buffer's slot for source p
+};
+
+__device__ __forceinline__ uint64_t gt() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint64_t* stamps) {
+  if (threadIdx.x == 0) stamps[3 * blockIdx.x] = gt();
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    for (int j = 1; j < P; ++j) {
+      const int q = (me + j) % P;
+      asm volatile("st.volatile.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(pr.slot[q] + i),
+                   "r"(val));
+    }
+  }
+  if (threadIdx.x == 0) stamps[3 * blockIdx.x + 1] = gt();
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    for (int j = 1; j < P; ++j) {
+      const int q = (me + j) % P;
+      while (true) {
+        uint4 v;
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(pr.in[q] + i));
+        if (v.x == val && v.w == val) break;
+        __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) stamps[3 * blockIdx.x + 2] = gt();
+}
+
+__global__ void ping(volatile uint64_t* mine, volatile uint64_t* theirs, int iters, int init,
+                     uint64_t* out) {
+  uint64_t s = 0, r = 0;
+  for (int i = 1; i <= iters; ++i) {
+    if (init) {
+      s = gt();
+      *theirs = i;
+    }
+    while (*mine != (uint64_t)i) {
+    }
+    r = gt();
+    if (!init) *theirs = i;
+  }
+  out[0] = s;
+  out[1] = r;
+}
+
+int main() {
+  int P = 0;
+  CK(cudaGetDeviceCount(&P));
+  P = std::min(P, kMaxP);
+  if (P < 2) return 0;
+  const uint64_t slot_bytes = 4ull << 20;
+  std::vector<uint4*> buf(P);
+  std::vector<uint64_t*> st(P), flag(P), out(P);
+  std::vector<cudaStream_t> s(P);
+  for (int g = 0; g < P; ++g) {
+    CK(cudaSetDevice(g));
+    for (int h = 0; h < P; ++h)
+      if (h != g) CK(cudaDeviceEnablePeerAccess(h, 0));
+    CK(cudaMalloc(&buf[g], slot_bytes * P));
+    CK(cudaMalloc(&st[g], 1 << 16));
+    CK(cudaMalloc(&flag[g], 64));
+    CK(cudaMalloc(&out[g], 64));
+    CK(cudaMemset(flag[g], 0, 64));
+    CK(cudaStreamCreateWithFlags(&s[g], cudaStreamNonBlocking));
+  }
+  // timer offsets vs GPU0
+  std::vector<double> off(P, 0.0);
+  for (int g = 1; g < P; ++g) {
+    CK(cudaSetDevice(g));
+    ping<<<1, 1, 0, s[g]>>>(flag[g], flag[0], 100, 0, out[g]);
+    CK(cudaSetDevice(0));
+    ping<<<1, 1, 0, s[0]>>>(flag[0], flag[g], 100, 1, out[0]);
+    CK(cudaStreamSynchronize(s[0]));
+    CK(cudaSetDevice(g));
+    CK(cudaStreamSynchronize(s[g]));
+    uint64_t a[2], b[2];
+    CK(cudaMemcpy(a, out[0], 16, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b, out[g], 16, cudaMemcpyDeviceToHost));
+    off[g] = (double)b[1] - ((double)a[0] + (double)a[1]) / 2.0;
+    CK(cudaSetDevice(0));
+    CK(cudaMemset(flag[0], 0, 64));
+    CK(cudaSetDevice(g));
+    CK(cudaMemset(flag[g], 0, 64));
+  }
+  printf("P=%d\n", P);
+  uint32_t val = 0x40000000u;
+  for (uint64_t bytes : {16ull << 10, 128ull << 10, 512ull << 10, 2048ull << 10}) {
+    for (int grid : {16, 32, 64, 128}) {
+      std::vector<double> tot, iss;
+      for (int rep = 0; rep < 5; ++rep) {
+        ++val;
+        for (int g = 0; g < P; ++g) {
+          CK(cudaSetDevice(g));
+          CK(cudaMemset(buf[g], 0xFF, slot_bytes * P));
+          CK(cudaDeviceSynchronize());
+        }
+        for (int g = 0; g < P; ++g) {
+          Peers pr{};
+          for (int q = 0; q < P; ++q) {
+            pr.slot[q] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(buf[q]) + g * slot_bytes);
+            pr.in[q] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(buf[g]) + q * slot_bytes);
+          }
+          CK(cudaSetDevice(g));
+          exch<<<grid, 512, 0, s[g]>>>(pr, g, P, bytes / 16, val, st[g]);
+        }
+        double t0 = 1e30, t_end = 0, iss_end = 0;
+        for (int g = 0; g < P; ++g) {
+          CK(cudaSetDevice(g));
+          CK(cudaStreamSynchronize(s[g]));
+          std::vector<uint64_t> h(3 * grid);
+          CK(cudaMemcpy(h.data(), st[g], 24 * grid, cudaMemcpyDeviceToHost));
+          for (int b = 0; b < grid; ++b) {
+            t0 = std::min(t0, (double)h[3 * b] - off[g]);
+            iss_end = std::max(iss_end, (double)h[3 * b + 1] - off[g]);
+            t_end = std::max(t_end, (double)h[3 * b + 2] - off[g]);
+          }
+        }
+        tot.push_back((t_end - t0) / 1e3);
+        iss.push_back((iss_end - t0) / 1e3);
+      }
+      std::sort(tot.begin(), tot.end());
+      std::sort(iss.begin(), iss.end());
+      printf("bytes/peer=%8llu grid=%4d : pushes issued by %.3f us, all arrived by %.3f us (p50)\n",
+             (unsigned long long)bytes, grid, iss[2], tot[2]);
+    }
+  }
+  return 0;
+}
