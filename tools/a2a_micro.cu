@@ -26,6 +26,8 @@ constexpr int kMaxP = 8;
 struct Peers {
   uint4* slot[kMaxP];  // slot[p] = my slot inside GPU p's buffer (for my pushes)
   uint4* in[kMaxP];    // my buffer's slot for source p
+  volatile uint32_t* ready;     // on GPU0: ready[g]
+  volatile uint32_t* go[kMaxP]; // go word on each GPU
 };
 
 __device__ __forceinline__ uint64_t gt() {
@@ -35,7 +37,20 @@ __device__ __forceinline__ uint64_t gt() {
 }
 
 __global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint64_t* stamps) {
-  if (threadIdx.x == 0) stamps[3 * blockIdx.x] = gt();
+  // start barrier across GPUs so launch skew does not count
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) pr.ready[me] = val;
+    if (me == 0 && blockIdx.x == 0) {
+      for (int g = 0; g < P; ++g)
+        while (pr.ready[g] != val) {
+        }
+      for (int g = 0; g < P; ++g) *pr.go[g] = val;
+    }
+    while (*pr.go[me] != val) {
+    }
+    stamps[3 * blockIdx.x] = gt();
+  }
+  __syncthreads();
   for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cells;
        i += (uint64_t)gridDim.x * blockDim.x) {
     for (int j = 1; j < P; ++j) {
@@ -88,6 +103,8 @@ int main() {
   const uint64_t slot_bytes = 4ull << 20;
   std::vector<uint4*> buf(P);
   std::vector<uint64_t*> st(P), flag(P), out(P);
+  std::vector<uint32_t*> gow(P);
+  uint32_t* ready = nullptr;
   std::vector<cudaStream_t> s(P);
   for (int g = 0; g < P; ++g) {
     CK(cudaSetDevice(g));
@@ -99,6 +116,12 @@ int main() {
     CK(cudaMalloc(&out[g], 64));
     CK(cudaMemset(flag[g], 0, 64));
     CK(cudaStreamCreateWithFlags(&s[g], cudaStreamNonBlocking));
+    CK(cudaMalloc(&gow[g], 64));
+    CK(cudaMemset(gow[g], 0, 64));
+    if (g == 0) {
+      CK(cudaMalloc(&ready, 256));
+      CK(cudaMemset(ready, 0, 256));
+    }
   }
   // timer offsets vs GPU0
   std::vector<double> off(P, 0.0);
@@ -137,6 +160,8 @@ int main() {
             pr.slot[q] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(buf[q]) + g * slot_bytes);
             pr.in[q] = reinterpret_cast<uint4*>(reinterpret_cast<char*>(buf[g]) + q * slot_bytes);
           }
+          pr.ready = ready;
+          for (int q = 0; q < P; ++q) pr.go[q] = gow[q];
           CK(cudaSetDevice(g));
           exch<<<grid, 512, 0, s[g]>>>(pr, g, P, bytes / 16, val, st[g]);
         }
