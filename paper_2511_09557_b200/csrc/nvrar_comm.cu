@@ -182,7 +182,8 @@ int validate_args(const nvrar_init_args* a) {
 // the message. `table` (from nvrar_set_plan_table, measured on the running
 // system) overrides it.
 void default_plan(int world, int nodes, uint64_t bytes, bool emu, int* algo, int* blocks) {
-  const uint64_t one_max = world <= 4 ? (512u << 10) : (256u << 10);
+  // one-shot moves (P-1)*M into every GPU: cheapest while that stays small
+  const uint64_t one_max = world <= 4 ? (1u << 20) : (256u << 10);
   if (world == 1) {
     *algo = NVRAR_ALGO_ONESHOT;
   } else if (emu) {
@@ -194,13 +195,7 @@ void default_plan(int world, int nodes, uint64_t bytes, bool emu, int* algo, int
   } else {
     *algo = NVRAR_ALGO_TWOSHOT;
   }
-  if (bytes <= (256u << 10)) {
-    *blocks = 32;
-  } else if (bytes <= (512u << 10)) {
-    *blocks = 64;
-  } else {
-    *blocks = 128;
-  }
+  *blocks = bytes <= (256u << 10) ? 64 : 128;
 }
 
 void plan_shape(int world, int nodes, int gpus, int algo_pref, int blocks_pref, int max_ctas,
