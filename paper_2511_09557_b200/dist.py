@@ -38,7 +38,10 @@ def max_over_ranks(values: Sequence[float], group=None, device: Optional[torch.d
                    ) -> List[float]:
     """Elementwise max over ranks of per-sample times (µs or ms)."""
     backend = dist.get_backend(group)
-    dev = device if (device is not None and backend == "nccl") else torch.device("cpu")
+    if backend == "nccl":
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    else:
+        dev = torch.device("cpu")
     t = torch.tensor(list(values), dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t.cpu().tolist()
