@@ -38,6 +38,25 @@ NVLINK_NOMINAL_GBS = 900.0  # NVLink 5 per direction per GPU
 SWEEP = [64 << 10, 128 << 10, 256 << 10, 512 << 10, 1 << 20, 2 << 20, 4 << 20, 8 << 20]
 
 
+def profiled_traffic(kernel_prefix):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
+    ncu --set full capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_hier_emu_metrics.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        if not p["kernel"].startswith(kernel_prefix):
+            return None
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            m = p["metrics"][k]
+            tot += float(m["value"]) * scale.get(m["unit"], 1)
+        return int(tot)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -216,9 +235,11 @@ def run_emulated(args):
                    "p90_us": round(per_call_us[(9 * len(per_call_us)) // 10], 3)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "peak_kind": hbm_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "traffic": None, "algorithmic_bytes": alg_bytes,
+                     "traffic": profiled_traffic("nvrar::hier_kernel") if algo == "hier" else None,
+                     "algorithmic_bytes": alg_bytes,
                      "note": "virtual ranks share one HBM: 2*P*M bytes (all inputs read, all "
-                             "outputs written) per launch"},
+                             "outputs written) per launch; traffic = DRAM bytes of one launch "
+                             "from profiles/r01_ncu_hier_emu_metrics.json (outputs stay in L2)"},
         "cpu_baseline": {"value": round(cpu_v, 3), "unit": "us", "cores": cpu_cores,
                          "kind": cpu_kind, "sample": cpu_sample},
         "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
