@@ -36,7 +36,8 @@ __device__ __forceinline__ uint64_t gt() {
   return t;
 }
 
-__global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint64_t* stamps) {
+__global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint64_t* stamps,
+                     int sleep_ns, int leader) {
   // start barrier across GPUs so launch skew does not count
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) pr.ready[me] = val;
@@ -64,13 +65,30 @@ __global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint
        i += (uint64_t)gridDim.x * blockDim.x) {
     for (int j = 1; j < P; ++j) {
       const int q = (me + j) % P;
+      if (leader) {
+        // lane 31's cell first (one poller per warp), then every lane checks its own
+        const uint64_t last = i - (threadIdx.x & 31) + 31;
+        if ((threadIdx.x & 31) == 31 || last >= cells) {
+        }
+        if ((threadIdx.x & 31) == 0 && last < cells) {
+          while (true) {
+            uint4 v;
+            asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "l"(pr.in[q] + last));
+            if (v.x == val && v.w == val) break;
+            if (sleep_ns) __nanosleep(sleep_ns);
+          }
+        }
+        __syncwarp();
+      }
       while (true) {
         uint4 v;
         asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                      : "l"(pr.in[q] + i));
         if (v.x == val && v.w == val) break;
-        __nanosleep(32);
+        if (sleep_ns) __nanosleep(sleep_ns);
       }
     }
   }
@@ -144,8 +162,12 @@ int main() {
   }
   printf("P=%d\n", P);
   uint32_t val = 0x40000000u;
+  for (int variant = 0; variant < 5; ++variant) {
+  const int sleep_ns = variant == 0 ? 0 : variant == 1 ? 32 : variant == 2 ? 256 : variant == 3 ? 1000 : 32;
+  const int leader = variant == 4;
+  printf("-- poll sleep %d ns%s\n", sleep_ns, leader ? ", warp-leader poll" : "");
   for (uint64_t bytes : {16ull << 10, 128ull << 10, 512ull << 10, 2048ull << 10}) {
-    for (int grid : {16, 32, 64, 128}) {
+    for (int grid : {32, 128}) {
       std::vector<double> tot, iss;
       for (int rep = 0; rep < 5; ++rep) {
         ++val;
@@ -163,7 +185,7 @@ int main() {
           pr.ready = ready;
           for (int q = 0; q < P; ++q) pr.go[q] = gow[q];
           CK(cudaSetDevice(g));
-          exch<<<grid, 512, 0, s[g]>>>(pr, g, P, bytes / 16, val, st[g]);
+          exch<<<grid, 512, 0, s[g]>>>(pr, g, P, bytes / 16, val, st[g], sleep_ns, leader);
         }
         double t0 = 1e30, t_end = 0, iss_end = 0;
         for (int g = 0; g < P; ++g) {
@@ -185,6 +207,7 @@ int main() {
       printf("bytes/peer=%8llu grid=%4d : pushes issued by %.3f us, all arrived by %.3f us (p50)\n",
              (unsigned long long)bytes, grid, iss[2], tot[2]);
     }
+  }
   }
   return 0;
 }
