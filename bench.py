@@ -39,22 +39,25 @@ SWEEP = [64 << 10, 128 << 10, 256 << 10, 512 << 10, 1 << 20, 2 << 20, 4 << 20, 8
 
 
 def profiled_traffic(kernel_prefix):
-    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
-    ncu --set full capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_hier_emu_metrics.json")
-    try:
-        with open(path) as fh:
-            p = json.load(fh)
-        if not p["kernel"].startswith(kernel_prefix):
-            return None
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        tot = 0.0
-        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            m = p["metrics"][k]
-            tot += float(m["value"]) * scale.get(m["unit"], 1)
-        return int(tot)
-    except Exception:
-        return None
+    """DRAM bytes (read + write) per launch of the dominant kernel from the newest
+    committed ncu --set full capture of that kernel (profiles/*_metrics.json), or None."""
+    import glob
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu*_metrics.json")),
+                       reverse=True):
+        try:
+            with open(path) as fh:
+                p = json.load(fh)
+            if not p["kernel"].startswith(kernel_prefix):
+                continue
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                m = p["metrics"][k]
+                tot += float(m["value"]) * scale.get(m["unit"], 1)
+            return int(tot), os.path.basename(path)
+        except Exception:
+            continue
+    return None, None
 
 
 def peaks():
@@ -159,7 +162,7 @@ def run_emulated(args):
 
     # the selector's choice for this shape, and each schedule forced (context)
     by_algo = {}
-    for algo in ("hier", "twoshot", "oneshot"):
+    for algo in ("hier", "twoshot", "oneshot", "direct"):
         g.set_algo(algo)
         gr = graph_for()
         ts = H.time_replays(gr.replay, max(3, args.steps // 2), 2, lambda: None, stream)
@@ -219,6 +222,8 @@ def run_emulated(args):
     g.check()
 
     cpu_v, cpu_kind, cpu_cores, cpu_sample = cpu_reference(nodes, gpus, n)
+    kname = {"hier": "hier", "twoshot": "flat", "oneshot": "flat", "direct": "direct"}[algo]
+    traffic, traffic_src = profiled_traffic(f"nvrar::{kname}_kernel")
     line = {
         "metric": METRIC, "value": round(p50, 3), "unit": "us", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup,
@@ -235,11 +240,11 @@ def run_emulated(args):
                    "p90_us": round(per_call_us[(9 * len(per_call_us)) // 10], 3)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "peak_kind": hbm_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "traffic": profiled_traffic("nvrar::hier_kernel") if algo == "hier" else None,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes": alg_bytes,
                      "note": "virtual ranks share one HBM: 2*P*M bytes (all inputs read, all "
                              "outputs written) per launch; traffic = DRAM bytes of one launch "
-                             "from profiles/r01_ncu_hier_emu_metrics.json (outputs stay in L2)"},
+                             "of the chosen schedule's kernel from the committed ncu capture"},
         "cpu_baseline": {"value": round(cpu_v, 3), "unit": "us", "cores": cpu_cores,
                          "kind": cpu_kind, "sample": cpu_sample},
         "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",

@@ -85,7 +85,11 @@ typedef enum {
   NVRAR_ALGO_AUTO = 0,
   NVRAR_ALGO_HIER = 1,
   NVRAR_ALGO_TWOSHOT = 2,
-  NVRAR_ALGO_ONESHOT = 3
+  NVRAR_ALGO_ONESHOT = 3,
+  /* virtual ranks sharing ONE device (nvrar_allreduce_local with every rank
+   * present): no exchange — each unit is folded once, in the same order, from
+   * all ranks' inputs and written to every rank's output. Elsewhere: HIER. */
+  NVRAR_ALGO_DIRECT = 4
 } nvrar_algo_t;
 
 /* Wire protocol. Both are self-validating (arrival of data = arrival of its

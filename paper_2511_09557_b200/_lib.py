@@ -24,9 +24,9 @@ ERR_NOT_CONNECTED = 7
 
 INT32, FLOAT32, BF16 = 0, 1, 2
 SUM = 0
-ALGO_AUTO, ALGO_HIER, ALGO_TWOSHOT, ALGO_ONESHOT = 0, 1, 2, 3
+ALGO_AUTO, ALGO_HIER, ALGO_TWOSHOT, ALGO_ONESHOT, ALGO_DIRECT = 0, 1, 2, 3, 4
 ALGO_NAMES = {ALGO_AUTO: "auto", ALGO_HIER: "hier", ALGO_TWOSHOT: "twoshot",
-              ALGO_ONESHOT: "oneshot"}
+              ALGO_ONESHOT: "oneshot", ALGO_DIRECT: "direct"}
 
 PROTO_AUTO, PROTO_LL, PROTO_LAMPORT = 0, 1, 2
 PROTO_CODES = {"auto": PROTO_AUTO, "ll": PROTO_LL, "lamport": PROTO_LAMPORT}

@@ -172,7 +172,7 @@ class NvrarConfig:
 
 _DTYPES = {torch.float32: L.FLOAT32, torch.bfloat16: L.BF16, torch.int32: L.INT32}
 _ALGOS = {"auto": L.ALGO_AUTO, "hier": L.ALGO_HIER, "twoshot": L.ALGO_TWOSHOT,
-          "oneshot": L.ALGO_ONESHOT}
+          "oneshot": L.ALGO_ONESHOT, "direct": L.ALGO_DIRECT}
 
 
 def dtype_code(t: torch.dtype) -> int:

@@ -20,6 +20,7 @@ namespace nvrar {
 using KernelFn = void (*)(LaunchParams);
 KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu, bool lamport);
 KernelFn bump_kernel();
+KernelFn select_direct(int dtype, int nodes);
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);
 PingFn pingpong_fn();
 int flat_max_gpus(int nodes);
@@ -187,7 +188,9 @@ void default_plan(int world, int nodes, uint64_t bytes, bool emu, int* algo, int
   if (world == 1) {
     *algo = NVRAR_ALGO_ONESHOT;
   } else if (emu) {
-    *algo = NVRAR_ALGO_HIER;  // virtual ranks share one HBM: least traffic wins
+    // virtual ranks share one HBM: no exchange at all (falls back to HIER
+    // when not every rank takes part in the launch)
+    *algo = NVRAR_ALGO_DIRECT;
   } else if (bytes <= one_max) {
     *algo = NVRAR_ALGO_ONESHOT;
   } else if (bytes <= (2u << 20) && nodes > 1) {
@@ -219,6 +222,7 @@ void plan_shape(int world, int nodes, int gpus, int algo_pref, int blocks_pref, 
   if (b <= 0) b = da == a ? db : std::max(db, 16);
   if ((a == NVRAR_ALGO_TWOSHOT || a == NVRAR_ALGO_ONESHOT) && !flat_ok) a = NVRAR_ALGO_HIER;
   if (a == NVRAR_ALGO_ONESHOT && bytes > kOneshotMaxBytes) a = NVRAR_ALGO_TWOSHOT;
+  if (a == NVRAR_ALGO_DIRECT && !emu) a = NVRAR_ALGO_HIER;
   b = std::max(1, std::min(b, max_ctas));
   *algo = a;
   *blocks = b;
@@ -484,7 +488,7 @@ int nvrar_set_config(nvrar_comm_t c, int blocks, uint64_t chunk_bytes) {
 }
 
 int nvrar_set_algo(nvrar_comm_t c, nvrar_algo_t algo) {
-  if (!c || algo < NVRAR_ALGO_AUTO || algo > NVRAR_ALGO_ONESHOT) {
+  if (!c || algo < NVRAR_ALGO_AUTO || algo > NVRAR_ALGO_DIRECT) {
     return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad algo");
   }
   if ((algo == NVRAR_ALGO_TWOSHOT || algo == NVRAR_ALGO_ONESHOT) &&
@@ -599,11 +603,15 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   int algo = 0, blocks = 1;
   plan(c0, count, dtype, &algo, &blocks, local_group && nl > 1);
   const bool emu = local_group;
+  // the direct schedule needs every rank of the topology in this launch
+  if (algo == NVRAR_ALGO_DIRECT && (!emu || nl != c0->world)) algo = NVRAR_ALGO_HIER;
   if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
   if (!emu) lp.d0 = c0->h_desc;  // by value: the kernel reads it from param space
   const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
-  KernelFn k = select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu, lamport);
+  KernelFn k = algo == NVRAR_ALGO_DIRECT
+                   ? select_direct(dtype, c0->nodes)
+                   : select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu, lamport);
   if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
 
   cudaLaunchConfig_t cfg{};

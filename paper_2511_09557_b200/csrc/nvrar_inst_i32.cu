@@ -6,4 +6,5 @@ KernelFn kernel_i32(bool flat, int nodes, bool emu, bool lamport) {
   (void)lamport;  // int32 has no spare bit pattern: always LL
   return kernel_for<I32, false>(flat, nodes, emu);
 }
+KernelFn kernel_direct_i32(int nodes) { return direct_for<I32>(nodes); }
 }  // namespace nvrar

@@ -627,7 +627,114 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   end_call(d, c.seq);
 }
 
+// ---------------------------------------------------------------------------
+// Direct schedule for virtual ranks that share one HBM (EMU launches with every
+// rank present): there is nothing to exchange, so each unit of the vector is
+// folded once — in the same reference order — from all ranks' inputs and
+// written to every rank's output. CTA (b, y) covers slice y of the units; the
+// per-rank call counters advance exactly as with the message-passing schedules.
+template <class E, int N, int MAXG>
+__global__ void __launch_bounds__(kThreads, 1) direct_kernel(const __grid_constant__ LaunchParams lp) {
+  using A = typename E::acc;
+  constexpr int UE = 16 / E::kBytes;
+  constexpr int RDW = 4;
+  constexpr int kLevels = Log2<N>::value + 1;
+  const RankDesc& d = *lp.desc[blockIdx.y];
+  begin_wait(d);
+  Ctl c;
+  if (!begin_seq(d, c)) return;
+  const uint32_t n = static_cast<uint32_t>(lp.count);
+  const int G = d.gpus, P = lp.nlocal;
+  const uint32_t SG = (n + G - 1) / G;
+  const uint64_t U = (n + UE - 1) / UE;
+  const uint64_t slice = (U + P - 1) / P;
+  const uint64_t s0 = slice * blockIdx.y;
+  const uint64_t s1 = s0 + slice < U ? s0 + slice : U;
+  const uint64_t ub = s0 + (s1 - s0) * blockIdx.x / gridDim.x;
+  const uint64_t ue = s0 + (s1 - s0) * (blockIdx.x + 1) / gridDim.x;
+  for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+    const uint32_t e0 = UE * static_cast<uint32_t>(u);
+    const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+    const int c0 = static_cast<int>(e0 / SG);
+    const bool straddle = e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG;
+    int l0 = c0 + 1;
+    if (l0 >= G) l0 -= G;
+    uint32_t r[N][MAXG][RDW];
+#pragma unroll
+    for (int nn = 0; nn < N; ++nn) {
+      int l = l0;
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        if (j < G) {
+          load_raw<E, UE>(lp.send[nn * G + l], e0, valid, r[nn][j]);
+          l = l + 1 == G ? 0 : l + 1;
+        }
+      }
+    }
+    A stack[kLevels][UE];
+#pragma unroll
+    for (int nn = 0; nn < N; ++nn) {
+      A v[UE];
+      if (!straddle) {
+        raw_to_acc<UE>(E{}, r[nn][0], v);
+#pragma unroll
+        for (int j = 1; j < MAXG; ++j) {
+          if (j < G) {
+            A a[UE];
+            raw_to_acc<UE>(E{}, r[nn][j], a);
+#pragma unroll
+            for (int q = 0; q < UE; ++q) v[q] = acc_add(v[q], a[q]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < UE; ++q) {
+          const int cq = q < valid ? static_cast<int>((e0 + q) / SG) : c0;
+          const int rot = cq - c0;
+          A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % G, q);
+#pragma unroll
+          for (int j = 1; j < MAXG; ++j) {
+            if (j < G) x = acc_add(x, pick<E, UE, RDW, N, MAXG>(r, nn, (j + rot) % G, q));
+          }
+          v[q] = x;
+        }
+      }
+      int lvl = 0;
+#pragma unroll
+      for (int k = 0; k < kLevels - 1; ++k) {
+        if (((nn >> k) & 1) && lvl == k) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) v[q] = acc_add(stack[k][q], v[q]);
+          lvl = k + 1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kLevels; ++k) {
+        if (k == lvl) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) stack[k][q] = v[q];
+        }
+      }
+    }
+    uint32_t o[RDW];
+    acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
+    for (int r2 = 0; r2 < P; ++r2) store_raw<E, UE>(lp.recv[r2], e0, valid, o);
+  }
+  end_call(d, c.seq);
+}
+
 using KernelFn = void (*)(LaunchParams);
+
+template <class E>
+KernelFn direct_for(int nodes) {
+  switch (nodes) {
+    case 1: return direct_kernel<E, 1, 8>;
+    case 2: return direct_kernel<E, 2, 8>;
+    case 4: return direct_kernel<E, 4, 8>;
+    case 8: return direct_kernel<E, 8, 4>;
+    default: return nullptr;
+  }
+}
 
 template <class E, bool LAMPORT, bool EMU>
 KernelFn hier_for(int nodes) {
@@ -660,5 +767,8 @@ KernelFn kernel_for(bool flat, int nodes, bool emu) {
 KernelFn kernel_f32(bool flat, int nodes, bool emu, bool lamport);
 KernelFn kernel_bf16(bool flat, int nodes, bool emu, bool lamport);
 KernelFn kernel_i32(bool flat, int nodes, bool emu, bool lamport);
+KernelFn kernel_direct_f32(int nodes);
+KernelFn kernel_direct_bf16(int nodes);
+KernelFn kernel_direct_i32(int nodes);
 
 }  // namespace nvrar

@@ -58,6 +58,15 @@ KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu, bool lamport) 
   }
 }
 
+KernelFn select_direct(int dtype, int nodes) {
+  switch (dtype) {
+    case 0: return kernel_direct_i32(nodes);
+    case 1: return kernel_direct_f32(nodes);
+    case 2: return kernel_direct_bf16(nodes);
+    default: return nullptr;
+  }
+}
+
 KernelFn bump_kernel() { return seq_bump_kernel; }
 
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);

@@ -54,7 +54,7 @@ def main():
                    timeout_s=args.timeout)
     rng = random.Random(1234)
     sizes = [1, 7, 1000, 4099, 65536, 131072, 300001, 1 << 20]
-    algos = ["hier", "twoshot", "oneshot", "auto"]
+    algos = ["hier", "twoshot", "oneshot", "auto", "direct"]
     dtypes = [torch.bfloat16, torch.float32, torch.int32]
     total = world * (world + 1) // 2
     for it in range(args.calls):

@@ -24,7 +24,7 @@ from paper_2511_09557_b200 import (BlockedRank, ClusterTopology, DeadlockError, 
                                    InvalidArgumentError, LocalGroup, NvrarConfig)
 
 DEV = 0
-ALGOS = ["hier", "twoshot", "oneshot"]
+ALGOS = ["hier", "twoshot", "oneshot", "direct"]
 FLAT_MAXG = {1: 8, 2: 8, 4: 4, 8: 2}
 
 _groups = {}
@@ -98,7 +98,7 @@ HIERS = [(1, 1), (1, 2), (2, 1), (1, 4), (2, 2), (4, 1), (1, 8), (2, 4), (4, 2),
 @pytest.mark.parametrize("dtype,proto", [("f32", "lamport"), ("f32", "ll"), ("bf16", "lamport"),
                                          ("bf16", "ll"), ("i32", "auto")])
 def test_parity_hierarchies(nodes, gpus, algo, dtype, proto):
-    if algo != "hier" and not flat_ok(nodes, gpus):
+    if algo in ("twoshot", "oneshot") and not flat_ok(nodes, gpus):
         pytest.skip("flat schedules cover P <= 16 within MAXG")
     g = group(nodes, gpus)
     for n in (1, 7, 1031, 65539):
