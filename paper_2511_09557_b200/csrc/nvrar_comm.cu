@@ -79,6 +79,8 @@ struct nvrar_comm {
   int sticky = 0;
   std::string last_error;
   int max_ctas = 148;  // co-resident CTAs of one kernel on this device
+  int sms = 148;
+  int direct_ctas[3] = {148, 148, 148};  // co-resident direct-schedule CTAs per dtype
   bool pdl = true;     // programmatic dependent launch for single-rank launches
   int proto = NVRAR_PROTO_AUTO;
   int threads = kThreads;  // threads per CTA (multiple of 32, <= kThreads)
@@ -322,6 +324,16 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
     }
   }
   c->max_ctas = std::max(1, std::min(kSeqSlots, sms * std::max(occ, 1)));
+  c->sms = sms;
+  for (int dt = 0; dt < 3; ++dt) {
+    int o = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &o, reinterpret_cast<const void*>(select_direct(dt, c->nodes)), kDirectThreads, 0) !=
+        cudaSuccess) {
+      o = 1;
+    }
+    c->direct_ctas[dt] = sms * std::max(o, 1);
+  }
   if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_THREADS")) {
     const int t = atoi(v);
@@ -605,9 +617,25 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   const bool emu = local_group;
   // the direct schedule needs every rank of the topology in this launch
   if (algo == NVRAR_ALGO_DIRECT && (!emu || nl != c0->world)) algo = NVRAR_ALGO_HIER;
-  if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  const bool direct = algo == NVRAR_ALGO_DIRECT;
+  if (direct) {
+    // no CTA waits on another: one thread per 16-byte unit, several waves allowed
+    // units per rank; at least one CTA per SM across the ranks while every CTA
+    // keeps >= a warp of units, at most one unit per thread
+    const size_t upr = ((count * dtype_bytes(dtype) + 15) / 16 + nl - 1) / nl;
+    const size_t full = (upr + kDirectThreads - 1) / kDirectThreads;
+    const size_t spread = std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
+    // ... and no more CTAs than fit at once (threads loop, prefetching the next unit)
+    const size_t resident = std::max(1, c0->direct_ctas[dtype] / nl);
+    blocks = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>({std::max(full, spread), resident, static_cast<size_t>(kSeqSlots)})));
+  } else if (emu) {
+    blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  }
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
-  if (!emu) lp.d0 = c0->h_desc;  // by value: the kernel reads it from param space
+  // by value: the kernel reads it from param space (EMU: only the topology fields
+  // are shared by the virtual ranks; each reads the rest through desc[])
+  lp.d0 = c0->h_desc;
   const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
   KernelFn k = algo == NVRAR_ALGO_DIRECT
                    ? select_direct(dtype, c0->nodes)
@@ -616,13 +644,13 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
 
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(blocks, nl);
-  cfg.blockDim = dim3(c0->threads);
+  cfg.blockDim = dim3(direct ? kDirectThreads : c0->threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   cfg.attrs = attr;
   cfg.numAttrs = 0;
-  if (emu) {
+  if (emu && !direct) {
     // virtual ranks wait on each other: all CTAs must be co-resident
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;

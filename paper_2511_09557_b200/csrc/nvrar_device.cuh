@@ -30,6 +30,7 @@ namespace nvrar {
 constexpr int kMaxRanks = 64;   // NVRAR_MAX_RANKS
 constexpr int kMaxLocal = 32;   // NVRAR_MAX_LOCAL (virtual ranks per launch)
 constexpr int kThreads = 512;   // threads per CTA
+constexpr int kDirectThreads = 256;  // direct schedule (no waits; several CTAs per SM)
 
 enum Status : uint32_t {
   kOk = 0,

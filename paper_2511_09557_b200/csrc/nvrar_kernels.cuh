@@ -99,8 +99,12 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
 }
 
 __device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
-  if (threadIdx.x == 0) {
-    for (int i = blockIdx.x; i < kSeqSlots; i += gridDim.x) d.state->seq[i] = seq;
+  // CTA b owns slots b, b + grid, ...; warp 0 writes them (small grids own many)
+  if (threadIdx.x < 32) {
+    for (int i = blockIdx.x + static_cast<int>(threadIdx.x) * gridDim.x; i < kSeqSlots;
+         i += 32 * gridDim.x) {
+      d.state->seq[i] = seq;
+    }
   }
   stamp(d, 6);
 }
@@ -634,32 +638,32 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 // written to every rank's output. CTA (b, y) covers slice y of the units; the
 // per-rank call counters advance exactly as with the message-passing schedules.
 template <class E, int N, int MAXG>
-__global__ void __launch_bounds__(kThreads, 1) direct_kernel(const __grid_constant__ LaunchParams lp) {
+__global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
   constexpr int UE = 16 / E::kBytes;
   constexpr int RDW = 4;
   constexpr int kLevels = Log2<N>::value + 1;
   const RankDesc& d = *lp.desc[blockIdx.y];
   begin_wait(d);
-  Ctl c;
-  if (!begin_seq(d, c)) return;
   const uint32_t n = static_cast<uint32_t>(lp.count);
-  const int G = d.gpus, P = lp.nlocal;
+  const int G = lp.d0.gpus, P = lp.nlocal;  // param space: no dependent load
   const uint32_t SG = (n + G - 1) / G;
-  const uint64_t U = (n + UE - 1) / UE;
-  const uint64_t slice = (U + P - 1) / P;
-  const uint64_t s0 = slice * blockIdx.y;
-  const uint64_t s1 = s0 + slice < U ? s0 + slice : U;
-  const uint64_t ub = s0 + (s1 - s0) * blockIdx.x / gridDim.x;
-  const uint64_t ue = s0 + (s1 - s0) * (blockIdx.x + 1) / gridDim.x;
-  for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-    const uint32_t e0 = UE * static_cast<uint32_t>(u);
+  const uint32_t U = (n + UE - 1) / UE;
+  const uint32_t slice = (U + P - 1) / P;
+  // small vectors leave the last ranks' slices empty (s0 clamps to U)
+  const uint32_t s0 = slice * blockIdx.y < U ? slice * blockIdx.y : U;
+  const uint32_t s1 = s0 + slice < U ? s0 + slice : U;
+  const uint32_t ub = s0 + static_cast<uint32_t>(static_cast<uint64_t>(s1 - s0) * blockIdx.x / gridDim.x);
+  const uint32_t ue = s0 + static_cast<uint32_t>(static_cast<uint64_t>(s1 - s0) * (blockIdx.x + 1) / gridDim.x);
+
+  uint32_t r[N][MAXG][RDW];
+  // loads of unit u from every rank, in each node's fold order (starting at the
+  // chunk after the unit's own, ring.hpp fold order)
+  auto load_unit = [&](uint32_t u) {
+    const uint32_t e0 = UE * u;
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
-    const int c0 = static_cast<int>(e0 / SG);
-    const bool straddle = e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG;
-    int l0 = c0 + 1;
+    int l0 = static_cast<int>(e0 / SG) + 1;
     if (l0 >= G) l0 -= G;
-    uint32_t r[N][MAXG][RDW];
 #pragma unroll
     for (int nn = 0; nn < N; ++nn) {
       int l = l0;
@@ -671,6 +675,17 @@ __global__ void __launch_bounds__(kThreads, 1) direct_kernel(const __grid_consta
         }
       }
     }
+  };
+  uint32_t u = ub + threadIdx.x;
+  // the first unit's loads do not depend on the call number: issue them first
+  if (u < ue) load_unit(u);
+  Ctl c;
+  if (!begin_seq(d, c)) return;
+  while (u < ue) {
+    const uint32_t e0 = UE * u;
+    const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+    const int c0 = static_cast<int>(e0 / SG);
+    const bool straddle = e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG;
     A stack[kLevels][UE];
 #pragma unroll
     for (int nn = 0; nn < N; ++nn) {
@@ -699,6 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) direct_kernel(const __grid_consta
           v[q] = x;
         }
       }
+      // pairwise tree over nodes in node order (XOR-step adds)
       int lvl = 0;
 #pragma unroll
       for (int k = 0; k < kLevels - 1; ++k) {
@@ -718,6 +734,8 @@ __global__ void __launch_bounds__(kThreads, 1) direct_kernel(const __grid_consta
     }
     uint32_t o[RDW];
     acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
+    u += blockDim.x;
+    if (u < ue) load_unit(u);
     for (int r2 = 0; r2 < P; ++r2) store_raw<E, UE>(lp.recv[r2], e0, valid, o);
   }
   end_call(d, c.seq);
