@@ -169,7 +169,7 @@ def run_emulated(args):
         by_algo[algo] = round(statistics.median(ts) * 1e3 / calls, 3)
         del gr
     g.set_algo("auto")
-    algo, blocks = g.comms[0].plan(n, torch.float32)
+    algo, blocks = g.plan(n, torch.float32)
     graph = graph_for()
     hbm, hbm_kind = peaks()
     with H.ClockSampler(0) as clk:
@@ -217,7 +217,7 @@ def run_emulated(args):
                             c2, stream)
             ts = H.time_replays(gr.replay, max(5, args.steps // 2), 2, lambda: None, stream)
             sweep[f"{size >> 10}KB_bf16"] = {"p50_us": round(statistics.median(ts) * 1e3 / c2, 3),
-                                             "algo": g.comms[0].plan(ne, torch.bfloat16)[0]}
+                                             "algo": g.plan(ne, torch.bfloat16)[0]}
             del gr, st
     g.check()
 

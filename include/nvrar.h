@@ -178,6 +178,10 @@ int nvrar_set_timeout(nvrar_comm_t comm, double timeout_s);
 int nvrar_set_protocol(nvrar_comm_t comm, nvrar_proto_t proto);
 /* Selected schedule and CTA count for a message (what nvrar_allreduce runs). */
 int nvrar_plan(nvrar_comm_t comm, size_t count, nvrar_dtype_t dtype, int* algo, int* blocks);
+/* The same for an nvrar_allreduce_local launch of the active comms (virtual
+ * ranks of one device may take the DIRECT schedule). */
+int nvrar_plan_local(nvrar_comm_t* comms, int ncomms, size_t count, nvrar_dtype_t dtype,
+                     uint64_t active_mask, int* algo, int* blocks);
 /* Install a measured selector table (ascending max_bytes; messages larger than
  * the last row fall back to the built-in policy). All ranks must install the
  * same table — paper_2511_09557_b200.selector.autotune() measures it with a

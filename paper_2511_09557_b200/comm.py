@@ -420,6 +420,16 @@ class LocalGroup:
         for c in self.comms:
             c.set_protocol(proto)
 
+    def plan(self, count: int, dtype: torch.dtype, active: Optional[Sequence[int]] = None):
+        """(schedule, CTAs per rank) a launch of this group runs for `count` elements."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        mask = (1 << 64) - 1 if active is None else sum(1 << r for r in active)
+        rc = self._lib.nvrar_plan_local(self._arr, self.topo.world_size(), count,
+                                        dtype_code(dtype), mask, ctypes.byref(a), ctypes.byref(b))
+        if rc:
+            _raise(rc, self.comms[0].last_error())
+        return L.ALGO_NAMES[a.value], b.value
+
     def launch(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
                active: Optional[Sequence[int]] = None,
                stream: Optional[torch.cuda.Stream] = None) -> None:

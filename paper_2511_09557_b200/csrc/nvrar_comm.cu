@@ -535,6 +535,21 @@ int nvrar_plan(nvrar_comm_t c, size_t count, nvrar_dtype_t dtype, int* algo, int
   return NVRAR_SUCCESS;
 }
 
+static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, int* algo_out,
+                    int* blocks_out);
+
+int nvrar_plan_local(nvrar_comm_t* comms, int ncomms, size_t count, nvrar_dtype_t dtype,
+                     uint64_t active_mask, int* algo, int* blocks) {
+  if (!comms || ncomms < 1 || ncomms > NVRAR_MAX_LOCAL || !comms[0] || !algo || !blocks ||
+      dtype < NVRAR_INT32 || dtype > NVRAR_BF16) {
+    return fail(comms ? comms[0] : nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad plan query");
+  }
+  int nl = 0;
+  for (int i = 0; i < ncomms; ++i) nl += static_cast<int>((active_mask >> i) & 1ull);
+  resolve(comms[0], std::max(nl, 1), count, dtype, true, algo, blocks);
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_set_plan_table(nvrar_comm_t c, const nvrar_plan_entry* entries, int n) {
   if (!c || n < 0 || (n > 0 && !entries)) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad table");
   std::vector<nvrar_plan_entry> t(entries, entries + n);
@@ -568,6 +583,31 @@ int nvrar_get_peers(nvrar_comm_t c, int* peers, int max_peers, int* steps) {
     peers[l] = ((node ^ (1 << l)) * c->gpus) + local;  // nvrar.hpp:72-75
   }
   return NVRAR_SUCCESS;
+}
+
+// The schedule and CTAs per rank a launch of nl ranks of c0's topology uses
+// (emu: the ranks are virtual ranks of one local group, one launch).
+static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, int* algo_out,
+                    int* blocks_out) {
+  int algo = 0, blocks = 1;
+  plan(c0, count, dtype, &algo, &blocks, emu && nl > 1);
+  // the direct schedule needs every rank of the topology in this launch
+  if (algo == NVRAR_ALGO_DIRECT && (!emu || nl != c0->world)) algo = NVRAR_ALGO_HIER;
+  if (algo == NVRAR_ALGO_DIRECT) {
+    // no CTA waits on another: units per rank spread over at least one CTA per
+    // SM while every CTA keeps >= a warp of units, at most one unit per thread,
+    // and no more CTAs than fit at once (threads loop, prefetching the next unit)
+    const size_t upr = ((count * dtype_bytes(dtype) + 15) / 16 + nl - 1) / nl;
+    const size_t full = (upr + kDirectThreads - 1) / kDirectThreads;
+    const size_t spread = std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
+    const size_t resident = std::max(1, c0->direct_ctas[dtype] / nl);
+    blocks = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>({std::max(full, spread), resident, static_cast<size_t>(kSeqSlots)})));
+  } else if (emu) {
+    blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  }
+  *algo_out = algo;
+  *blocks_out = blocks;
 }
 
 static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void* const* recv,
@@ -613,25 +653,9 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
     return NVRAR_SUCCESS;
   }
   int algo = 0, blocks = 1;
-  plan(c0, count, dtype, &algo, &blocks, local_group && nl > 1);
   const bool emu = local_group;
-  // the direct schedule needs every rank of the topology in this launch
-  if (algo == NVRAR_ALGO_DIRECT && (!emu || nl != c0->world)) algo = NVRAR_ALGO_HIER;
+  resolve(c0, nl, count, dtype, emu, &algo, &blocks);
   const bool direct = algo == NVRAR_ALGO_DIRECT;
-  if (direct) {
-    // no CTA waits on another: one thread per 16-byte unit, several waves allowed
-    // units per rank; at least one CTA per SM across the ranks while every CTA
-    // keeps >= a warp of units, at most one unit per thread
-    const size_t upr = ((count * dtype_bytes(dtype) + 15) / 16 + nl - 1) / nl;
-    const size_t full = (upr + kDirectThreads - 1) / kDirectThreads;
-    const size_t spread = std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
-    // ... and no more CTAs than fit at once (threads loop, prefetching the next unit)
-    const size_t resident = std::max(1, c0->direct_ctas[dtype] / nl);
-    blocks = static_cast<int>(std::max<size_t>(
-        1, std::min<size_t>({std::max(full, spread), resident, static_cast<size_t>(kSeqSlots)})));
-  } else if (emu) {
-    blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
-  }
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
   // by value: the kernel reads it from param space (EMU: only the topology fields
   // are shared by the virtual ranks; each reads the rest through desc[])

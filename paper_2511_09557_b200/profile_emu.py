@@ -50,7 +50,7 @@ def main():
     for _ in range(args.calls):
         g.launch(ins, outs)
     g.check()
-    print("plan", g.comms[0].plan(n, dt), "ok")
+    print("plan", g.plan(n, dt), "ok")
     g.close()
 
 

@@ -72,11 +72,11 @@ def main():
         xs = [(idx * (r + 1)).to(dt) for r in range(world)]
         ys = [torch.empty_like(x) for x in xs]
         if args.verbose:
-            print(it, algo, blocks, dt, n, g.comms[0].plan(n, dt), flush=True)
+            print(it, algo, blocks, dt, n, g.plan(n, dt), flush=True)
         try:
             g.run_all(xs, ys)
         except Exception as e:  # noqa: BLE001
-            print(f"call {it} ({algo}/{blocks} {dt} n={n} plan={g.comms[0].plan(n, dt)}): {e}")
+            print(f"call {it} ({algo}/{blocks} {dt} n={n} plan={g.plan(n, dt)}): {e}")
             for b in getattr(e, "blocked", lambda: [])():
                 dump_cell(g, b, args, world, n, ys, dt)
             return 1
@@ -90,7 +90,7 @@ def main():
             for r, c in enumerate(g.comms):
                 cnt, first = c.dirty_cells()
                 if cnt:
-                    print(f"call {it} ({algo}/{blocks} {dt} n={n} plan={g.comms[0].plan(n, dt)}): "
+                    print(f"call {it} ({algo}/{blocks} {dt} n={n} plan={g.plan(n, dt)}): "
                           f"rank {r} left {cnt} non-empty slot words (first at byte {first})")
                     return 1
     print(f"OK after {args.calls} calls")

@@ -290,3 +290,7 @@ def test_peers_and_sequence_api():
     assert [(p.node_rank, p.local_rank) for p in peers] == [(3, 1), (0, 1)]
     algo, blocks = g.comms[0].plan(1 << 20, torch.bfloat16)
     assert algo in ALGOS and blocks >= 1
+    # a full local group of virtual ranks may take the direct schedule
+    la, lb = g.plan(1 << 20, torch.bfloat16)
+    assert la in ALGOS and lb >= 1
+    assert g.plan(1 << 20, torch.bfloat16, active=[0, 1])[0] != "direct"
