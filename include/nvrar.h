@@ -171,6 +171,43 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
                           void* const* recv, size_t count, nvrar_dtype_t dtype, nvrar_op_t op,
                           void* stream, uint64_t active_mask);
 
+/* ---- phase-only entry points --------------------------------------------
+ * One phase of the hierarchical all-reduce on its own, run by the same kernel
+ * code as nvrar_allreduce (debugging and phase-level parity). Each call
+ * consumes one sequence number of the comm, like an all-reduce; all ranks must
+ * issue the same sequence of calls. Participants are the rank's node group
+ * (local ranks 0..gpus_per_node-1 of its node), in local-rank order. */
+typedef enum {
+  NVRAR_PHASE_ALL = 0,             /* the full all-reduce */
+  NVRAR_PHASE_REDUCE_SCATTER = 1,  /* IntraReduceScatter<T>::run (nvrar.hpp:280-299) */
+  NVRAR_PHASE_RD_INTER = 2,        /* NvrarAllreduce<T>::rd_inter (nvrar.hpp:132-155) */
+  NVRAR_PHASE_ALL_GATHER = 3       /* IntraAllGather<T>::run (nvrar.hpp:348-364) */
+} nvrar_phase_t;
+
+/* Node-local sum of `count` elements; this rank (local rank g) receives chunk g
+ * of the zero-padded vector: ceil(count / gpus_per_node) elements, in the
+ * reference's fold order. count == 0 is INVALID_ARGUMENT (nvrar.hpp:282-284);
+ * members' counts must agree, else PROTOCOL_FAULT. */
+int nvrar_reduce_scatter(nvrar_comm_t comm, const void* send, void* recv_shard, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
+/* Concatenate the node members' `shard_count`-element shards in local-rank
+ * order into recv (gpus_per_node * shard_count elements). Shard lengths must
+ * agree, else PROTOCOL_FAULT (collectives_test.cpp:226-237). */
+int nvrar_all_gather(nvrar_comm_t comm, const void* shard, void* recv, size_t shard_count,
+                     nvrar_dtype_t dtype, void* stream);
+/* Inter-node recursive doubling only. `packed` holds this rank's shard as LL
+ * words (data = low 32 bits, flag = high 32 bits) packed with sequence()+1;
+ * `out` receives the reduced shard packed with that call number. A flag other
+ * than the call's is PROTOCOL_FAULT. dtype: INT32 or FLOAT32. With one node
+ * the words are copied unchanged (nvrar.hpp:140-143). */
+int nvrar_rd_inter(nvrar_comm_t comm, const uint64_t* packed, uint64_t* out, size_t words,
+                   nvrar_dtype_t dtype, void* stream);
+/* The phase entry points for the virtual ranks of one device (as
+ * nvrar_allreduce_local); `phase` is an nvrar_phase_t. */
+int nvrar_phase_local(nvrar_comm_t* comms, int ncomms, int phase, const void* const* send,
+                      void* const* recv, size_t count, nvrar_dtype_t dtype, void* stream,
+                      uint64_t active_mask);
+
 /* ---- config / introspection -------------------------------------------- */
 int nvrar_set_config(nvrar_comm_t comm, int blocks, uint64_t chunk_bytes);
 int nvrar_set_algo(nvrar_comm_t comm, nvrar_algo_t algo);

@@ -130,6 +130,60 @@ static int is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 DEFINE_ORDER_SUM(orc_nvrar_order_sum_f32, float, add_f32)
 DEFINE_ORDER_SUM(orc_nvrar_order_sum_i32, int32_t, add_i32)
 
+/* ---- standalone phases ---------------------------------------------------
+ * intra_rs_sum (tests/oracles.hpp:89-97): the node members' inputs zero-padded
+ * to ce*G (ce = ceil(n/G)); chunk c of the result is ring_chunk_fold(c) =
+ * x[(c+1)%G] + ... + x[c] (oracles.hpp:49-61). Output: ce*G elements.
+ * rd_inter (NvrarAllreduce::rd_inter, nvrar.hpp:132-155): every rank (node, g)
+ * holds a w-element shard; the result for local rank g is the XOR-step sum over
+ * nodes, v[node] = v[node^bit] + v[node] (rd_block, nvrar.hpp:197-220), the same
+ * bits on every node. inputs/out: P x w, rank-major. */
+#define DEFINE_INTRA_RS(NAME, T, ADD)                                               \
+  int NAME(int gpus, size_t n, const T* inputs, T* out) {                           \
+    if (gpus < 1) return -2;                                                        \
+    if (n == 0) return 0;                                                           \
+    const size_t ce = (n + (size_t)gpus - 1) / (size_t)gpus;                        \
+    for (size_t e = 0; e < ce * (size_t)gpus; ++e) {                                \
+      const int c = (int)(e / ce);                                                  \
+      if (e >= n) {                                                                 \
+        out[e] = (T)0;                                                              \
+        continue;                                                                   \
+      }                                                                             \
+      T f = inputs[(size_t)((c + 1) % gpus) * n + e];                               \
+      for (int j = 2; j < gpus; ++j) f = ADD(f, inputs[(size_t)((c + j) % gpus) * n + e]); \
+      if (gpus > 1) f = ADD(f, inputs[(size_t)c * n + e]);                          \
+      out[e] = f;                                                                   \
+    }                                                                               \
+    return 0;                                                                       \
+  }
+
+#define DEFINE_RD_INTER(NAME, T, ADD)                                               \
+  int NAME(int nodes, int gpus, size_t w, const T* shards, T* out) {                \
+    if (nodes < 1 || gpus < 1) return -2;                                           \
+    if (!is_pow2(nodes) || nodes > ORC_MAX_NODES) return -1;                        \
+    T v[ORC_MAX_NODES], nx[ORC_MAX_NODES];                                          \
+    for (int g = 0; g < gpus; ++g) {                                                \
+      for (size_t i = 0; i < w; ++i) {                                              \
+        for (int node = 0; node < nodes; ++node) {                                  \
+          v[node] = shards[((size_t)node * (size_t)gpus + (size_t)g) * w + i];      \
+        }                                                                           \
+        for (int bit = 1; bit < nodes; bit <<= 1) {                                 \
+          for (int node = 0; node < nodes; ++node) nx[node] = ADD(v[node ^ bit], v[node]); \
+          memcpy(v, nx, sizeof(T) * (size_t)nodes);                                 \
+        }                                                                           \
+        for (int node = 0; node < nodes; ++node) {                                  \
+          out[((size_t)node * (size_t)gpus + (size_t)g) * w + i] = v[node];         \
+        }                                                                           \
+      }                                                                             \
+    }                                                                               \
+    return 0;                                                                       \
+  }
+
+DEFINE_INTRA_RS(orc_intra_rs_sum_f32, float, add_f32)
+DEFINE_INTRA_RS(orc_intra_rs_sum_i32, int32_t, add_i32)
+DEFINE_RD_INTER(orc_rd_inter_f32, float, add_f32)
+DEFINE_RD_INTER(orc_rd_inter_i32, int32_t, add_i32)
+
 /* ---- bf16 -------------------------------------------------------------- */
 float orc_bf16_to_f32(uint16_t b) {
   uint32_t u = (uint32_t)b << 16;

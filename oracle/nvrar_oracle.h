@@ -59,6 +59,13 @@ int orc_nvrar_order_sum_bf16(int nodes, int gpus, size_t n, const uint16_t* inpu
                              uint16_t* out);
 
 /* oracles::serial_sum: global-rank order. */
+/* Standalone phases: intra_rs_sum (tests/oracles.hpp:89-97; out = ce*G
+ * elements) and the rd_inter result (nvrar.hpp:132-155; P x w rank-major). */
+int orc_intra_rs_sum_f32(int gpus, size_t n, const float* inputs, float* out);
+int orc_intra_rs_sum_i32(int gpus, size_t n, const int32_t* inputs, int32_t* out);
+int orc_rd_inter_f32(int nodes, int gpus, size_t w, const float* shards, float* out);
+int orc_rd_inter_i32(int nodes, int gpus, size_t w, const int32_t* shards, int32_t* out);
+
 void orc_serial_sum_f32(int ranks, size_t n, const float* inputs, float* out);
 void orc_serial_sum_i32(int ranks, size_t n, const int32_t* inputs, int32_t* out);
 

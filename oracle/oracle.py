@@ -54,6 +54,12 @@ def lib():
                      "orc_nvrar_order_sum_bf16"):
             getattr(L, name).argtypes = [ctypes.c_int, ctypes.c_int, c_sz, vp, vp]
             getattr(L, name).restype = ctypes.c_int
+        for name in ("orc_intra_rs_sum_f32", "orc_intra_rs_sum_i32"):
+            getattr(L, name).argtypes = [ctypes.c_int, c_sz, vp, vp]
+            getattr(L, name).restype = ctypes.c_int
+        for name in ("orc_rd_inter_f32", "orc_rd_inter_i32"):
+            getattr(L, name).argtypes = [ctypes.c_int, ctypes.c_int, c_sz, vp, vp]
+            getattr(L, name).restype = ctypes.c_int
         L.orc_serial_sum_f32.argtypes = [ctypes.c_int, c_sz, vp, vp]
         L.orc_serial_sum_i32.argtypes = [ctypes.c_int, c_sz, vp, vp]
         L.orc_make_word.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
@@ -92,6 +98,13 @@ def ref():
         R.ref_nvrar_stalled_rank.argtypes = [ci, ci, c_sz, ci, c_u64, c_u64, vp, ci,
                                              ctypes.POINTER(ci), ctypes.c_char_p, c_sz]
         R.ref_nvrar_stalled_rank.restype = ci
+        for name in ("ref_intra_rs_f32", "ref_intra_rs_i32", "ref_intra_ag_f32",
+                     "ref_intra_ag_i32"):
+            getattr(R, name).argtypes = [ci, ci, c_sz, vp, vp, ctypes.c_char_p, c_sz]
+            getattr(R, name).restype = ci
+        for name in ("ref_rd_inter_f32", "ref_rd_inter_i32"):
+            getattr(R, name).argtypes = [ci, ci, c_sz, vp, vp, ci, c_u64, ctypes.c_char_p, c_sz]
+            getattr(R, name).restype = ci
         _ref = R
     return _ref
 
@@ -148,6 +161,49 @@ def nvrar_order_sum(inputs: np.ndarray, nodes: int, gpus: int, dtype: str = "f32
     if rc != 0:
         raise RuntimeError(f"oracle rc={rc}")
     return out
+
+
+def intra_rs_sum(node_inputs: np.ndarray) -> np.ndarray:
+    """tests/oracles.hpp:89-97: the node-local ring reduce-scatter result,
+    zero-padded to ceil(n/G)*G elements (chunk g = local rank g's shard)."""
+    x = np.ascontiguousarray(node_inputs)
+    g, n = x.shape
+    name = {np.dtype(np.float32): "orc_intra_rs_sum_f32", np.dtype(np.int32): "orc_intra_rs_sum_i32"}[x.dtype]
+    out = np.empty(-(-n // g) * g, x.dtype)
+    if getattr(lib(), name)(g, n, _ptr(x), _ptr(out)) != 0:
+        raise RuntimeError("oracle intra_rs_sum failed")
+    return out
+
+
+def rd_inter(shards: np.ndarray, nodes: int, gpus: int) -> np.ndarray:
+    """NvrarAllreduce::rd_inter result (nvrar.hpp:132-155): per local rank, the
+    XOR-step sum of its node peers' shards. shards: [P, w] -> [P, w]."""
+    x = np.ascontiguousarray(shards)
+    p, w = x.shape
+    assert p == nodes * gpus
+    name = {np.dtype(np.float32): "orc_rd_inter_f32", np.dtype(np.int32): "orc_rd_inter_i32"}[x.dtype]
+    out = np.empty_like(x)
+    rc = getattr(lib(), name)(nodes, gpus, w, _ptr(x), _ptr(out))
+    if rc == -1:
+        raise ValueError(f"nodes={nodes} is not a power of two")
+    if rc != 0:
+        raise RuntimeError(f"oracle rc={rc}")
+    return out
+
+
+def pack_fused(data_bits: np.ndarray, seq: int) -> np.ndarray:
+    """fused.hpp pack: word = data (low 32 bits) | seq << 32 (transport.hpp:81-87)."""
+    d = np.ascontiguousarray(data_bits).view(np.uint32).astype(np.uint64)
+    return d | (np.uint64(seq) << np.uint64(32))
+
+
+def unpack_fused(words: np.ndarray, seq: int, dtype=np.int32) -> np.ndarray:
+    """fused.hpp unpack: every flag must equal seq (else the reference throws)."""
+    w = np.ascontiguousarray(words).astype(np.uint64)
+    flags = (w >> np.uint64(32)).astype(np.uint32)
+    if np.any(flags != np.uint32(seq)):
+        raise ValueError("stale flag")
+    return (w & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(dtype)
 
 
 def serial_sum(inputs: np.ndarray) -> np.ndarray:
@@ -232,6 +288,36 @@ def ref_nvrar_run_all(inputs: np.ndarray, nodes: int, gpus: int, blocks: int = 1
         ref().ref_nvrar_run_all_i32
     rc = fn(nodes, gpus, inputs.shape[1], _ptr(inputs), _ptr(out), blocks, chunk_bytes,
             1 if concurrent else 0, seed, delay_us, timeout_s, err, 512)
+    if rc != 0:
+        raise RefError(rc, err.value.decode())
+    return out
+
+
+def ref_intra_phase(which: str, inputs: np.ndarray, nodes: int, gpus: int) -> np.ndarray:
+    """Every rank runs ccsim::IntraReduceScatter<T> ('rs': [P, n] -> [P, ceil(n/G)])
+    or IntraAllGather<T> ('ag': [P, ce] -> [P, G*ce]) with its node's members."""
+    x = np.ascontiguousarray(inputs)
+    p, ln = x.shape
+    out_len = -(-ln // gpus) if which == "rs" else ln * gpus
+    out = np.empty((p, out_len), x.dtype)
+    suffix = "f32" if x.dtype == np.float32 else "i32"
+    err = ctypes.create_string_buffer(512)
+    rc = getattr(ref(), f"ref_intra_{which}_{suffix}")(nodes, gpus, ln, _ptr(x), _ptr(out), err, 512)
+    if rc != 0:
+        raise RefError(rc, err.value.decode())
+    return out
+
+
+def ref_rd_inter(shards: np.ndarray, nodes: int, gpus: int, blocks: int = 1,
+                 chunk_bytes: int = 65536) -> np.ndarray:
+    """Every rank runs ccsim::NvrarAllreduce<T>::rd_inter on its fused-packed shard
+    (the collectives_test.cpp:286-302 driver); returns the unpacked [P, w] results."""
+    x = np.ascontiguousarray(shards)
+    out = np.empty_like(x)
+    suffix = "f32" if x.dtype == np.float32 else "i32"
+    err = ctypes.create_string_buffer(512)
+    rc = getattr(ref(), f"ref_rd_inter_{suffix}")(nodes, gpus, x.shape[1], _ptr(x), _ptr(out),
+                                                   blocks, chunk_bytes, err, 512)
     if rc != 0:
         raise RefError(rc, err.value.decode())
     return out

@@ -94,6 +94,66 @@ int run_all(int nodes, int gpus, std::size_t n, const T* inputs, T* outputs, int
   });
 }
 
+// The standalone phases through the reference's own classes on VirtualTime:
+// IntraReduceScatter / IntraAllGather with each node's members as participants
+// (nvrar.hpp:254-373), and NvrarAllreduce::rd_inter on fused-packed shards
+// (nvrar.hpp:132-155; the collectives_test.cpp:286-302 driver).
+template <Element T>
+int intra_phase(int which, int nodes, int gpus, std::size_t len, const T* inputs, T* outputs,
+                char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const ClusterTopology topo{nodes, gpus};
+    topo.validate();
+    const int ng = topo.world_size();
+    const std::size_t ce = which == 0 ? (len + gpus - 1) / gpus : len;
+    const std::size_t out_len = which == 0 ? ce : len * gpus;
+    auto in = unflatten(inputs, ng, len);
+    std::vector<std::vector<T>> out(ng, std::vector<T>(out_len));
+    auto program = [&](Ctx& ctx) -> Task {
+      const int me = ctx.global();
+      std::vector<RankId> mates;
+      for (int g = 0; g < gpus; ++g) mates.push_back(RankId{ctx.self().node_rank, g});
+      if (which == 0) {
+        IntraReduceScatter<T> rs(ctx, len, mates);
+        co_await rs.run(std::span<const T>(in[me]), std::span<T>(out[me]));
+      } else {
+        IntraAllGather<T> ag(ctx, len, mates);
+        co_await ag.run(std::span<const T>(in[me]), std::span<T>(out[me]));
+      }
+    };
+    run_ranks(topo, CostParams{}, TransportMode::VirtualTime, {}, program);
+    for (int r = 0; r < ng; ++r) {
+      std::memcpy(outputs + static_cast<std::size_t>(r) * out_len, out[r].data(),
+                  out_len * sizeof(T));
+    }
+  });
+}
+
+template <Element T>
+int rd_inter_all(int nodes, int gpus, std::size_t w, const T* shards, T* outputs, int blocks,
+                 std::uint64_t chunk, char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const ClusterTopology topo{nodes, gpus};
+    topo.validate();
+    const int ng = topo.world_size();
+    auto in = unflatten(shards, ng, w);
+    std::vector<std::vector<T>> out(ng);
+    const NvrarConfig cfg{blocks, chunk};
+    auto program = [&](Ctx& ctx) -> Task {
+      const int me = ctx.global();
+      NvrarAllreduce<T> st(ctx, w * ctx.topo().gpus_per_node);
+      auto packed = pack_fused<T>(in[me], st.sequence() + 1);
+      std::vector<std::uint64_t> reduced(w);
+      co_await st.rd_inter(packed, reduced, cfg);
+      out[me] = unpack_fused<T>(reduced, st.sequence());
+    };
+    run_ranks(topo, CostParams{}, TransportMode::VirtualTime, {}, program);
+    for (int r = 0; r < ng; ++r) {
+      std::memcpy(outputs + static_cast<std::size_t>(r) * w, out[r].data(), w * sizeof(T));
+    }
+  });
+}
+
 // Times NvrarAllreduce<T>::run on ConcurrentEngine with pre-generated inputs
 // (unlike run_bench_point, which generates inputs inside its timed loop,
 // bench.hpp:92-93). Per call: makespan = max over ranks of the wall time at
@@ -183,6 +243,32 @@ int ref_nvrar_run_all_i32(int nodes, int gpus, std::size_t n, const std::int32_t
                           std::size_t errlen) {
   return run_all<std::int32_t>(nodes, gpus, n, inputs, outputs, blocks, chunk, mode, seed,
                                delay_us, timeout_s, err, errlen);
+}
+
+int ref_intra_rs_f32(int nodes, int gpus, std::size_t n, const float* in, float* out, char* err,
+                     std::size_t errlen) {
+  return intra_phase<float>(0, nodes, gpus, n, in, out, err, errlen);
+}
+int ref_intra_rs_i32(int nodes, int gpus, std::size_t n, const std::int32_t* in,
+                     std::int32_t* out, char* err, std::size_t errlen) {
+  return intra_phase<std::int32_t>(0, nodes, gpus, n, in, out, err, errlen);
+}
+int ref_intra_ag_f32(int nodes, int gpus, std::size_t ce, const float* in, float* out, char* err,
+                     std::size_t errlen) {
+  return intra_phase<float>(1, nodes, gpus, ce, in, out, err, errlen);
+}
+int ref_intra_ag_i32(int nodes, int gpus, std::size_t ce, const std::int32_t* in,
+                     std::int32_t* out, char* err, std::size_t errlen) {
+  return intra_phase<std::int32_t>(1, nodes, gpus, ce, in, out, err, errlen);
+}
+int ref_rd_inter_f32(int nodes, int gpus, std::size_t w, const float* in, float* out, int blocks,
+                     std::uint64_t chunk, char* err, std::size_t errlen) {
+  return rd_inter_all<float>(nodes, gpus, w, in, out, blocks, chunk, err, errlen);
+}
+int ref_rd_inter_i32(int nodes, int gpus, std::size_t w, const std::int32_t* in,
+                     std::int32_t* out, int blocks, std::uint64_t chunk, char* err,
+                     std::size_t errlen) {
+  return rd_inter_all<std::int32_t>(nodes, gpus, w, in, out, blocks, chunk, err, errlen);
 }
 
 int ref_nvrar_time_concurrent_f32(int nodes, int gpus, std::size_t n, const float* inputs,

@@ -14,8 +14,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libnvrar_b200.so")
-SOURCES = ["nvrar_inst_f32.cu", "nvrar_inst_bf16.cu", "nvrar_inst_i32.cu", "nvrar_misc.cu",
-           "nvrar_comm.cu"]
+SOURCES = ["nvrar_inst_f32.cu", "nvrar_inst_bf16.cu", "nvrar_inst_i32.cu",
+           "nvrar_inst_phase_f.cu", "nvrar_inst_phase_i.cu", "nvrar_misc.cu", "nvrar_comm.cu"]
 HEADERS = ["nvrar_device.cuh", "nvrar_kernels.cuh", os.path.join("..", "..", "include", "nvrar.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

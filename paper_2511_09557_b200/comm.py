@@ -309,6 +309,33 @@ class Communicator:
         if rc:
             _raise(rc, self.last_error(), self.rank)
 
+    # ---- phase-only entry points (nvrar.h "phase-only entry points") ----------
+    def reduce_scatter(self, send: torch.Tensor, shard: torch.Tensor,
+                       stream: Optional[torch.cuda.Stream] = None) -> None:
+        """IntraReduceScatter<T>::run (nvrar.hpp:280-299): `shard` gets this rank's
+        ceil(n/G) elements of the node-local sum."""
+        _check_phase_io(PHASE_REDUCE_SCATTER, send, shard, self.topo.gpus_per_node)
+        self._check(self._lib.nvrar_reduce_scatter(self._h, send.data_ptr(), shard.data_ptr(),
+                                                   send.numel(), dtype_code(send.dtype), L.SUM,
+                                                   _stream_ptr(stream)))
+
+    def all_gather(self, shard: torch.Tensor, recv: torch.Tensor,
+                   stream: Optional[torch.cuda.Stream] = None) -> None:
+        """IntraAllGather<T>::run (nvrar.hpp:348-364): recv = the node members'
+        shards concatenated in local-rank order."""
+        _check_phase_io(PHASE_ALL_GATHER, shard, recv, self.topo.gpus_per_node)
+        self._check(self._lib.nvrar_all_gather(self._h, shard.data_ptr(), recv.data_ptr(),
+                                               shard.numel(), dtype_code(shard.dtype),
+                                               _stream_ptr(stream)))
+
+    def rd_inter(self, packed: torch.Tensor, out: torch.Tensor, dtype: torch.dtype = torch.int32,
+                 stream: Optional[torch.cuda.Stream] = None) -> None:
+        """NvrarAllreduce<T>::rd_inter (nvrar.hpp:132-155) on LL-packed int64 words."""
+        _check_phase_io(PHASE_RD_INTER, packed, out, self.topo.gpus_per_node)
+        self._check(self._lib.nvrar_rd_inter(self._h, packed.data_ptr(), out.data_ptr(),
+                                             packed.numel(), dtype_code(dtype),
+                                             _stream_ptr(stream)))
+
     def allreduce_raw(self, send_ptr: int, recv_ptr: int, count: int, dtype: int,
                       stream_ptr: int) -> None:
         rc = self._lib.nvrar_allreduce(self._h, send_ptr, recv_ptr, count, dtype, L.SUM,
@@ -348,6 +375,30 @@ def _check_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
         raise InvalidArgumentError("nvrar: buffers must be CUDA tensors")
     if not (send.is_contiguous() and recv.is_contiguous()):
         raise InvalidArgumentError("nvrar: buffers must be contiguous")
+
+
+PHASE_REDUCE_SCATTER, PHASE_RD_INTER, PHASE_ALL_GATHER = 1, 2, 3
+_PHASES = {"reduce_scatter": PHASE_REDUCE_SCATTER, "rd_inter": PHASE_RD_INTER,
+           "all_gather": PHASE_ALL_GATHER}
+
+
+def _check_phase_io(phase: int, src: torch.Tensor, dst: torch.Tensor, gpus: int) -> None:
+    if not (src.is_cuda and dst.is_cuda):
+        raise InvalidArgumentError("nvrar: buffers must be CUDA tensors")
+    if not (src.is_contiguous() and dst.is_contiguous()):
+        raise InvalidArgumentError("nvrar: buffers must be contiguous")
+    if src.dtype != dst.dtype:
+        raise InvalidArgumentError("nvrar: input and output dtypes differ")
+    n = src.numel()
+    if phase == PHASE_REDUCE_SCATTER and dst.numel() != -(-n // gpus):
+        raise InvalidArgumentError("intra reduce-scatter: shard output must be ceil(n/G)")
+    if phase == PHASE_ALL_GATHER and dst.numel() != n * gpus:
+        raise InvalidArgumentError("intra all-gather: output must be G * shard")
+    if phase == PHASE_RD_INTER:
+        if src.dtype != torch.int64:
+            raise InvalidArgumentError("rd_inter: packed words are int64 tensors")
+        if dst.numel() != n:
+            raise InvalidArgumentError("rd_inter: bad shard length")
 
 
 # ---- the reference-shaped collective ------------------------------------------------
@@ -461,6 +512,34 @@ class LocalGroup:
         for c, code in zip(self.comms, codes):
             if code:
                 _raise(code, c.last_error(), c.rank)
+
+    def launch_phase(self, phase: str, inputs: Sequence[torch.Tensor],
+                     outputs: Sequence[torch.Tensor], dtype: Optional[torch.dtype] = None,
+                     active: Optional[Sequence[int]] = None,
+                     stream: Optional[torch.cuda.Stream] = None) -> None:
+        """One phase-only launch for every virtual rank (nvrar_phase_local).
+        phase: 'reduce_scatter' | 'all_gather' | 'rd_inter' (dtype = the packed
+        words' element type, int32 or float32)."""
+        code = _PHASES[phase]
+        p = self.topo.world_size()
+        if len(inputs) != p or len(outputs) != p:
+            raise InvalidArgumentError("one input and one output per rank")
+        for a, b in zip(inputs, outputs):
+            _check_phase_io(code, a, b, self.topo.gpus_per_node)
+        dt = dtype_code(dtype if code == PHASE_RD_INTER else inputs[0].dtype)
+        send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
+        recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])
+        mask = (1 << 64) - 1 if active is None else sum(1 << r for r in active)
+        rc = self._lib.nvrar_phase_local(self._arr, p, code, send, recv, inputs[0].numel(), dt,
+                                         _stream_ptr(stream), mask)
+        if rc:
+            _raise(rc, self.comms[0].last_error())
+
+    def run_phase(self, phase: str, inputs: Sequence[torch.Tensor],
+                  outputs: Sequence[torch.Tensor], dtype: Optional[torch.dtype] = None,
+                  active: Optional[Sequence[int]] = None) -> None:
+        self.launch_phase(phase, inputs, outputs, dtype, active)
+        self.check()
 
     def run_all(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
                 cfg: Optional[NvrarConfig] = None, active: Optional[Sequence[int]] = None,

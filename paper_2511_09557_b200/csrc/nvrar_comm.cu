@@ -21,6 +21,7 @@ using KernelFn = void (*)(LaunchParams);
 KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu, bool lamport);
 KernelFn bump_kernel();
 KernelFn select_direct(int dtype, int nodes);
+KernelFn select_phase(int dtype, int mode, int nodes, bool emu);
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);
 PingFn pingpong_fn();
 int flat_max_gpus(int nodes);
@@ -610,12 +611,32 @@ static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, i
   *blocks_out = blocks;
 }
 
+// Bytes of the full-vector equivalent a call of `phase` moves (what max_bytes bounds).
+static size_t phase_bytes(const nvrar_comm* c, int phase, size_t count, int dtype) {
+  switch (phase) {
+    case NVRAR_PHASE_ALL_GATHER: return count * c->gpus * dtype_bytes(dtype);  // G shards
+    case NVRAR_PHASE_RD_INTER: return count * c->gpus * 4;  // one shard of 4-byte words
+    default: return count * dtype_bytes(dtype);
+  }
+}
+
 static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void* const* recv,
-                  size_t count, int dtype, int op, void* stream, uint64_t mask, bool local_group) {
+                  size_t count, int dtype, int op, void* stream, uint64_t mask, bool local_group,
+                  int phase = NVRAR_PHASE_ALL) {
   nvrar_comm* c0 = comms[0];
   if (op != NVRAR_SUM) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "only SUM is supported");
   if (dtype < NVRAR_INT32 || dtype > NVRAR_BF16) {
     return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  }
+  if (phase < NVRAR_PHASE_ALL || phase > NVRAR_PHASE_ALL_GATHER) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "bad phase %d", phase);
+  }
+  if (phase == NVRAR_PHASE_RD_INTER && dtype == NVRAR_BF16) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "rd_inter: packed words carry int32 or fp32");
+  }
+  // the standalone intra phases reject empty vectors (nvrar.hpp:282-284,350-352)
+  if (count == 0 && (phase == NVRAR_PHASE_REDUCE_SCATTER || phase == NVRAR_PHASE_ALL_GATHER)) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "intra phase: bad vector length 0");
   }
   LaunchParams lp{};
   int nl = 0;
@@ -627,10 +648,10 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
       return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "comms differ in device or topology");
     }
     if (int s = check_sticky(c)) return fail(c, s, "comm is in a failed state: %s", c->last_error.c_str());
-    if (count * dtype_bytes(dtype) > c->max_bytes) {
+    if (phase_bytes(c, phase, count, dtype) > c->max_bytes) {
       return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
                   "nvrar: vector longer than the preallocated maximum (%zu B > %zu B)",
-                  count * dtype_bytes(dtype), c->max_bytes);
+                  phase_bytes(c, phase, count, dtype), c->max_bytes);
     }
     if (count > 0 && (!send[i] || !recv[i])) {
       return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null buffer");
@@ -654,16 +675,23 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   }
   int algo = 0, blocks = 1;
   const bool emu = local_group;
-  resolve(c0, nl, count, dtype, emu, &algo, &blocks);
+  resolve(c0, nl, phase == NVRAR_PHASE_ALL ? count : phase_bytes(c0, phase, count, dtype) /
+                                                         dtype_bytes(dtype),
+          dtype, emu, &algo, &blocks);
+  if (phase != NVRAR_PHASE_ALL) {
+    // the phase-only entry points run the hierarchical kernel's phase code
+    algo = NVRAR_ALGO_HIER;
+    if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  }
   const bool direct = algo == NVRAR_ALGO_DIRECT;
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
   // by value: the kernel reads it from param space (EMU: only the topology fields
   // are shared by the virtual ranks; each reads the rest through desc[])
   lp.d0 = c0->h_desc;
   const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
-  KernelFn k = algo == NVRAR_ALGO_DIRECT
-                   ? select_direct(dtype, c0->nodes)
-                   : select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu, lamport);
+  KernelFn k = phase != NVRAR_PHASE_ALL ? select_phase(dtype, phase, c0->nodes, emu)
+               : direct ? select_direct(dtype, c0->nodes)
+                        : select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu, lamport);
   if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
 
   cudaLaunchConfig_t cfg{};
@@ -696,6 +724,43 @@ int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t coun
   const void* s[1] = {send};
   void* r[1] = {recv};
   return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false);
+}
+
+int nvrar_reduce_scatter(nvrar_comm_t comm, const void* send, void* recv_shard, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  const void* s[1] = {send};
+  void* r[1] = {recv_shard};
+  return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false,
+                NVRAR_PHASE_REDUCE_SCATTER);
+}
+
+int nvrar_all_gather(nvrar_comm_t comm, const void* shard, void* recv, size_t shard_count,
+                     nvrar_dtype_t dtype, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  const void* s[1] = {shard};
+  void* r[1] = {recv};
+  return launch(&comm, 1, s, r, shard_count, dtype, NVRAR_SUM, stream, ~0ull, false,
+                NVRAR_PHASE_ALL_GATHER);
+}
+
+int nvrar_rd_inter(nvrar_comm_t comm, const uint64_t* packed, uint64_t* out, size_t words,
+                   nvrar_dtype_t dtype, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  const void* s[1] = {packed};
+  void* r[1] = {out};
+  return launch(&comm, 1, s, r, words, dtype, NVRAR_SUM, stream, ~0ull, false,
+                NVRAR_PHASE_RD_INTER);
+}
+
+int nvrar_phase_local(nvrar_comm_t* comms, int ncomms, int phase, const void* const* send,
+                      void* const* recv, size_t count, nvrar_dtype_t dtype, void* stream,
+                      uint64_t active_mask) {
+  if (!comms || ncomms < 1 || ncomms > NVRAR_MAX_LOCAL || !send || !recv) {
+    return fail(comms ? comms[0] : nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad local group");
+  }
+  return launch(comms, ncomms, send, recv, count, dtype, NVRAR_SUM, stream, active_mask, true,
+                phase);
 }
 
 int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* send,

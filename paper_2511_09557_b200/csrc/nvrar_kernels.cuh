@@ -155,8 +155,27 @@ __device__ __forceinline__ int chunk_valid(uint64_t S, uint64_t u, uint64_t n, u
 constexpr int kHierMaxG = 8;
 constexpr int kHierUpt = 2;  // units per thread carried through the RD steps together
 
+// hier_kernel MODE: the full all-reduce, or one phase of it on its own (the
+// reference's standalone phases: IntraReduceScatter / IntraAllGather,
+// nvrar.hpp:254-373, and NvrarAllreduce::rd_inter, nvrar.hpp:133-155). The
+// phase-only modes run the very same phase code as the all-reduce.
+enum : int { kModeFull = 0, kModeRS = 1, kModeRD = 2, kModeAG = 3 };
+
+// Group members' length guard for the intra-only modes: publish (seq<<32|len)
+// to every other member and wait for theirs (the reference guard,
+// nvrar.hpp:324-336, checks the ring neighbour; every member is stricter).
+__device__ __forceinline__ void group_guard(Ctl& c, const RankDesc& d, uint64_t len) {
+  const int G = d.gpus;
+  if (G == 1) return;
+  const int t = static_cast<int>(threadIdx.x);
+  const int peer = d.node * G + (d.local + 1 + t) % G;
+  if (blockIdx.x == 0 && t < G - 1) publish_seq_len(d, peer, c.seq, len);
+  if (t < G - 1) wait_seq_len(c, d, peer, len);
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
-template <class E, bool LAMPORT, int N, bool EMU>
+template <class E, bool LAMPORT, int N, bool EMU, int MODE = kModeFull>
 __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
   using C = Cfg<E, LAMPORT>;
@@ -164,11 +183,18 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   using Part = typename C::Part;
   constexpr int UE = C::UE;
   constexpr int RDW = C::RDW;
-  constexpr int kSteps = Log2<N>::value;
+  constexpr bool kFull = MODE == kModeFull, kRS = MODE == kModeRS;
+  constexpr bool kRD = MODE == kModeRD, kAG = MODE == kModeAG;
+  constexpr bool kFold = kFull || kRS;    // phase 1 runs
+  constexpr bool kGather = kFull || kAG;  // phase 3 runs
+  constexpr int kSteps = (kFull || kRD) ? Log2<N>::value : 0;
+  static_assert(!kRD || (E::kBytes == 4 && UE == 4), "rd_inter moves 4-byte elements");
   const RankDesc& d = rank_desc<EMU>(lp);
-  const uint64_t n = lp.count;
   const int G = d.gpus, me = d.rank, node = d.node, local = d.local;
-  const uint64_t S = (n + G - 1) / G;
+  // full / RS: n = vector length, S = ceil(n/G); AG: count = shard, n = G * shard;
+  // RD: count = shard words, the shard is the whole vector (no chunking)
+  const uint64_t n = kAG ? lp.count * G : lp.count;
+  const uint64_t S = (kAG || kRD) ? lp.count : (n + G - 1) / G;
   const uint64_t U = (S + UE - 1) / UE;
   const uint64_t ub = U * blockIdx.x / gridDim.x;
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
@@ -188,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
   for (int j = 0; j < kHierMaxG; ++j) {
     pv[j] = 0;
-    if (j < G && u_first < ue) {
+    if (kFold && j < G && u_first < ue) {
       const uint64_t cbase = static_cast<uint64_t>(grp[j]) * S;
       pv[j] = chunk_valid<UE>(S, u_first, n, cbase);
       if (pv[j] > 0) load_raw<E, UE>(send, cbase + UE * u_first, pv[j], pre[j]);
@@ -204,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   }
 
   // Phase 1a: reduce-scatter pushes (ring_reduce_scatter_phase, ring_schedule.hpp:33-58).
-  if (G > 1) {
+  if (kFold && G > 1) {
 #pragma unroll
     for (int j = 1; j < kHierMaxG; ++j) {
       if (j < G && pv[j] > 0) {
@@ -236,11 +262,12 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
     __syncthreads();
   }
+  if constexpr (kRS || kAG) group_guard(c, d, lp.count);
   stamp(d, 3);
   c.phase = 4;
 
   // Phases 1b+2+3a: fold own chunk, recursive doubling, cast + all-gather push.
-  const uint64_t mybase = static_cast<uint64_t>(local) * S;
+  const uint64_t mybase = kRD ? 0 : static_cast<uint64_t>(local) * S;
   for (uint64_t u0 = ub + threadIdx.x; u0 < ue; u0 += static_cast<uint64_t>(blockDim.x) * kHierUpt) {
     A f[kHierUpt][UE];
     int valid[kHierUpt];
@@ -250,9 +277,31 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       uu[k] = u0 + static_cast<uint64_t>(k) * blockDim.x;
       valid[k] = uu[k] < ue ? chunk_valid<UE>(S, uu[k], n, mybase) : 0;
     }
+    if constexpr (kRD) {
+      // rd_inter input: this rank's shard packed as LL words {data, seq}; every
+      // flag must be this call's (nvrar.hpp:145-150); one node copies (:140-143)
+#pragma unroll
+      for (int k = 0; k < kHierUpt; ++k) {
+        if (valid[k] == 0) continue;
+        const uint64_t* in = static_cast<const uint64_t*>(send) + UE * uu[k];
+        uint32_t b[UE];
+#pragma unroll
+        for (int q = 0; q < UE; ++q) {
+          b[q] = 0u;
+          if (q < valid[k]) {
+            const uint64_t w = in[q];
+            b[q] = static_cast<uint32_t>(w);
+            if (N > 1 && static_cast<uint32_t>(w >> 32) != c.seq) {
+              record_fault(c, kProtocolFault, kStaleFlag, me, UE * uu[k] + q, w);
+            }
+          }
+        }
+        bits_acc<UE>(b, f[k]);
+      }
+    }
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
-      if (valid[k] == 0) continue;
+      if (!kFold || valid[k] == 0) continue;
       uint32_t own[RDW];
       if (k == 0 && u0 == u_first) {
 #pragma unroll
@@ -329,9 +378,37 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     // Final cast, own output, all-gather push (ring_all_gather_phase, ring_schedule.hpp:62-83).
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
+      if constexpr (kRS) {
+        // the shard is the whole output (IntraReduceScatter::run's `out`),
+        // padding past n included: zeros summed, i.e. +0 (nvrar.hpp:296-297)
+        if (uu[k] >= ue) continue;
+        uint32_t o[RDW];
+#pragma unroll
+        for (int q = 0; q < RDW; ++q) o[q] = 0u;
+        if (valid[k] > 0) acc_to_raw<UE>(E{}, f[k], o);
+        store_raw<E, UE>(recv, UE * uu[k], clamp_valid<UE>(static_cast<int64_t>(S) -
+                                                            static_cast<int64_t>(UE * uu[k])), o);
+        continue;
+      }
       if (valid[k] == 0) continue;
+      if constexpr (kRD) {
+        // packed result, flag = this call (rd_inter's out, nvrar.hpp:153)
+        uint32_t b[UE];
+        acc_bits<UE>(f[k], b);
+        uint64_t* out = static_cast<uint64_t*>(recv) + UE * uu[k];
+        const uint64_t* in = static_cast<const uint64_t*>(send) + UE * uu[k];
+#pragma unroll
+        for (int q = 0; q < UE; ++q) {
+          if (q < valid[k]) out[q] = N == 1 ? in[q] : (static_cast<uint64_t>(c.seq) << 32) | b[q];
+        }
+        continue;
+      }
       uint32_t o[RDW];
-      acc_to_raw<UE>(E{}, f[k], o);
+      if constexpr (kAG) {
+        load_raw<E, UE>(send, UE * uu[k], valid[k], o);  // the caller's shard
+      } else {
+        acc_to_raw<UE>(E{}, f[k], o);
+      }
       store_raw<E, UE>(recv, mybase + UE * uu[k], valid[k], o);
 #pragma unroll
       for (int j = 1; j < kHierMaxG; ++j) {
@@ -345,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   c.phase = 5;
 
   // Phase 3b: all-gather receive.
-  if (G > 1) {
+  if (kGather && G > 1) {
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
       uint32_t r[1][kHierMaxG - 1][RDW];
       uint4* slots[1][kHierMaxG - 1];
@@ -754,6 +831,17 @@ KernelFn direct_for(int nodes) {
   }
 }
 
+template <class E, bool LAMPORT, bool EMU, int MODE>
+KernelFn phase_for(int nodes) {
+  switch (nodes) {
+    case 1: return hier_kernel<E, LAMPORT, 1, EMU, MODE>;
+    case 2: return hier_kernel<E, LAMPORT, 2, EMU, MODE>;
+    case 4: return hier_kernel<E, LAMPORT, 4, EMU, MODE>;
+    case 8: return hier_kernel<E, LAMPORT, 8, EMU, MODE>;
+    default: return nullptr;
+  }
+}
+
 template <class E, bool LAMPORT, bool EMU>
 KernelFn hier_for(int nodes) {
   switch (nodes) {
@@ -788,5 +876,8 @@ KernelFn kernel_i32(bool flat, int nodes, bool emu, bool lamport);
 KernelFn kernel_direct_f32(int nodes);
 KernelFn kernel_direct_bf16(int nodes);
 KernelFn kernel_direct_i32(int nodes);
+KernelFn kernel_phase_f32(int mode, int nodes, bool emu);
+KernelFn kernel_phase_bf16(int mode, int nodes, bool emu);
+KernelFn kernel_phase_i32(int mode, int nodes, bool emu);
 
 }  // namespace nvrar

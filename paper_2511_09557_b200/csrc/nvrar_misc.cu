@@ -67,6 +67,15 @@ KernelFn select_direct(int dtype, int nodes) {
   }
 }
 
+KernelFn select_phase(int dtype, int mode, int nodes, bool emu) {
+  switch (dtype) {
+    case 0: return kernel_phase_i32(mode, nodes, emu);
+    case 1: return kernel_phase_f32(mode, nodes, emu);
+    case 2: return kernel_phase_bf16(mode, nodes, emu);
+    default: return nullptr;
+  }
+}
+
 KernelFn bump_kernel() { return seq_bump_kernel; }
 
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);

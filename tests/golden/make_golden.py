@@ -91,6 +91,21 @@ def main() -> None:
     g["stalled_4x1_rows"] = rows
     meta["stalled_4x1_msg"] = msg
 
+    # 7. standalone phases (collectives_test.cpp:179-354): IntraReduceScatter /
+    # IntraAllGather with each node's members, NvrarAllreduce::rd_inter.
+    g["rs_i32_1x2_hand"] = O.ref_intra_phase("rs", np.array([[1, 2], [3, 4]], np.int32), 1, 2)
+    for nodes, gpus, n, dt, seed in [(1, 4, 64, "i32", 17), (2, 4, 1031, "f32", 19),
+                                     (1, 3, 1000, "f32", 21), (2, 3, 4099, "f32", 23)]:
+        x = O.ref_random_inputs(nodes * gpus, n, seed, dt)
+        rs = O.ref_intra_phase("rs", x, nodes, gpus)
+        g[f"rs_{dt}_{nodes}x{gpus}_n{n}_s{seed}"] = rs
+        ag = O.ref_intra_phase("ag", rs, nodes, gpus)
+        meta[f"ag_{dt}_{nodes}x{gpus}_n{n}_s{seed}_sha256"] = sha(ag)
+    for nodes, gpus, w, dt, seed in [(8, 2, 96, "i32", 5), (4, 2, 777, "f32", 29),
+                                     (8, 1, 1000, "f32", 31), (2, 4, 100, "f32", 37)]:
+        x = O.ref_random_inputs(nodes * gpus, w, seed, dt)
+        g[f"rd_{dt}_{nodes}x{gpus}_w{w}_s{seed}"] = O.ref_rd_inter(x, nodes, gpus)
+
     np.savez_compressed(OUT, **g)
     with open(META, "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
