@@ -48,6 +48,8 @@ def main():
     ap.add_argument("--nodes", type=int, required=True)
     ap.add_argument("--gpus", type=int, required=True)
     ap.add_argument("--mismatch", action="store_true", help="length-mismatch protocol fault")
+    ap.add_argument("--ag-mismatch", action="store_true",
+                    help="all-gather shard-length mismatch (collectives_test.cpp:226-237)")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -67,6 +69,47 @@ def main():
         print(f"rank {rank}: mismatch status {rc} ({comm.last_error()})", flush=True)
         dist.barrier()
         sys.exit(0 if ok else 1)
+
+    if args.ag_mismatch:
+        shard = torch.ones(4 if rank == 0 else 3, dtype=torch.int32, device="cuda")
+        out = torch.empty(shard.numel() * args.gpus, dtype=torch.int32, device="cuda")
+        comm.all_gather(shard, out)
+        rc = comm.check_status()
+        print(f"rank {rank}: ag mismatch status {rc} ({comm.last_error()})", flush=True)
+        dist.barrier()
+        sys.exit(0 if rc == L.ERR_PROTOCOL_FAULT else 1)
+
+    # the phase-only entry points across processes (nvrar.h phase section)
+    G = args.gpus
+    node = rank // G
+    for dtype in ("f32", "i32"):
+        n = 4099
+        x = inputs(dtype, world, n, 900)
+        tdt = torch.float32 if dtype == "f32" else torch.int32
+        shard = torch.empty(-(-n // G), dtype=tdt, device="cuda")
+        comm.reduce_scatter(to_dev(x[rank], dtype), shard)
+        full = torch.empty(shard.numel() * G, dtype=tdt, device="cuda")
+        comm.all_gather(shard, full)
+        torch.cuda.synchronize()
+        comm.check()
+        want = O.intra_rs_sum(x[node * G:(node + 1) * G])
+        if not np.array_equal(full.cpu().numpy().view(np.uint32), want.view(np.uint32)):
+            fails += 1
+            print(f"rank {rank}: {dtype} reduce-scatter + all-gather differ", flush=True)
+        w = 777
+        sh = inputs(dtype, world, w, 901)
+        call = comm.sequence() + 1
+        packed = torch.from_numpy(O.pack_fused(sh[rank], call).view(np.int64)).cuda()
+        red = torch.empty_like(packed)
+        comm.rd_inter(packed, red, dtype=tdt)
+        torch.cuda.synchronize()
+        comm.check()
+        got = O.unpack_fused(red.cpu().numpy().view(np.uint64), call,
+                             np.float32 if dtype == "f32" else np.int32)
+        if not np.array_equal(got.view(np.uint32),
+                              O.rd_inter(sh, args.nodes, G)[rank].view(np.uint32)):
+            fails += 1
+            print(f"rank {rank}: {dtype} rd_inter differs", flush=True)
 
     algos = ["hier", "twoshot", "oneshot"]
     for dtype in ("f32", "bf16", "i32"):

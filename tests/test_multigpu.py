@@ -53,3 +53,12 @@ def test_length_mismatch_is_protocol_fault(nodes, gpus):
     rc, out = _run(2, nodes, gpus, ("--mismatch",))
     assert rc == 0, out[-4000:]
     assert "status 4" in out, out[-4000:]
+
+
+def test_all_gather_length_mismatch_is_protocol_fault():
+    """collectives_test.cpp:226-237 across processes: shard 4 vs 3 elements."""
+    if NDEV < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, 1, 2, ("--ag-mismatch",))
+    assert rc == 0, out[-4000:]
+    assert out.count("ag mismatch status 4") == 2, out[-4000:]
