@@ -1,0 +1,66 @@
+"""NVRAR as a CUDA-graph-capturable torch custom op.
+
+    comm = Communicator.from_process_group(topo, max_bytes)
+    cid = torch_op.register(comm)
+    y = torch.ops.nvrar.all_reduce(x, cid)      # out of place
+    torch.ops.nvrar.all_reduce_(x, cid)         # in place
+
+The op enqueues one nvrar_allreduce on the current stream (no host sync), so
+a model step that calls it can be captured in a CUDA graph and replayed; the
+call counter lives on the device and advances on every replay. The fake
+(meta) implementation lets torch.compile trace through it as an opaque op.
+"""
+from __future__ import annotations
+
+from typing import Dict
+
+import torch
+
+from .comm import Communicator
+
+_COMMS: Dict[int, Communicator] = {}
+
+
+def register(comm: Communicator) -> int:
+    """Make `comm` addressable from the op; returns its id."""
+    cid = len(_COMMS) + 1
+    _COMMS[cid] = comm
+    return cid
+
+
+def unregister(cid: int) -> None:
+    _COMMS.pop(cid, None)
+
+
+def _comm(cid: int) -> Communicator:
+    try:
+        return _COMMS[cid]
+    except KeyError:
+        raise ValueError(f"nvrar: no communicator registered under id {cid}") from None
+
+
+@torch.library.custom_op("nvrar::all_reduce", mutates_args=())
+def all_reduce(x: torch.Tensor, comm_id: int) -> torch.Tensor:
+    """Sum of `x` over every rank of the communicator (out of place)."""
+    src = x.contiguous()
+    out = torch.empty_like(src)
+    _comm(comm_id).allreduce(src, out)
+    return out
+
+
+@all_reduce.register_fake
+def _all_reduce_fake(x: torch.Tensor, comm_id: int) -> torch.Tensor:
+    return torch.empty_like(x, memory_format=torch.contiguous_format)
+
+
+@torch.library.custom_op("nvrar::all_reduce_", mutates_args=("x",))
+def all_reduce_(x: torch.Tensor, comm_id: int) -> None:
+    """In-place sum (send == recv is allowed)."""
+    if not x.is_contiguous():
+        raise ValueError("nvrar::all_reduce_: x must be contiguous")
+    _comm(comm_id).allreduce(x, x)
+
+
+@all_reduce_.register_fake
+def _all_reduce__fake(x: torch.Tensor, comm_id: int) -> None:
+    return None

@@ -1,0 +1,231 @@
+"""Tensor-parallel decode step driven by the Llama shapes.
+
+The caller of the hot path: the paper's end-to-end claim is decode-step time
+of a TP transformer whose layers each end two row-parallel projections with an
+all-reduce of the [batch, hidden] activations (attention out-projection and
+MLP down-projection; workload.hpp:91-117). This module
+builds that step on the GPUs of one node — one process per GPU — with the
+all-reduce supplied by either NVRAR (torch.ops.nvrar.all_reduce_) or NCCL
+(torch.distributed.all_reduce), captures the whole step (layers x 2
+all-reduces) in one CUDA graph, and times replays with CUDA events, max over
+ranks.
+
+Per layer and rank (Llama-3.1 shapes, bf16, random weights):
+    h  = rmsnorm(x) @ W_qkv[:, shard]         column-parallel (q, k, v heads / TP)
+    a  = h[:, :hidden/TP] @ W_o[shard, :]     row-parallel -> all-reduce #1
+    x  = x + a
+    g  = rmsnorm(x) @ W_gate_up[:, shard]     column-parallel (2 * ffn / TP)
+    d  = (silu(g1) * g2) @ W_down[shard, :]   row-parallel -> all-reduce #2
+    x  = x + d
+The attention kernel itself (KV-cache reads) is left out (the q-head slice
+stands in for its output): it does not touch the all-reduce and is the same
+for both arms; the step time
+reported is that of the GEMM + all-reduce skeleton, and the comm share is
+(step - step without all-reduce). Weights rotate over `weight_sets` copies so
+the per-layer reads come from HBM, not L2.
+
+    torchrun --nproc-per-node 4 -m paper_2511_09557_b200.tp_decode --model 70b
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+LLAMA = {
+    # Llama-3.1 configs: hidden, ffn (intermediate), q heads, kv heads, layers
+    "70b": dict(hidden=8192, ffn=28672, heads=64, kv_heads=8, layers=80),
+    "405b": dict(hidden=16384, ffn=53248, heads=128, kv_heads=8, layers=126),
+}
+
+
+@dataclass
+class DecodeWorkload:
+    """workload.hpp:22-35: batch x hidden activations of `bytes_per_element`."""
+
+    batch_size: int = 1
+    hidden_dim: int = 1
+    bytes_per_element: int = 2
+    num_layers: int = 1
+
+    def validate(self) -> None:
+        if self.batch_size < 1 or self.hidden_dim < 1 or self.num_layers < 1:
+            raise ValueError("workload: batch, hidden, layers must be >= 1")
+        if self.bytes_per_element not in (2, 4):
+            raise ValueError("workload: bytes_per_element must be 2 or 4")
+
+    def msg_bytes(self) -> int:
+        """decode_msg_bytes (workload.hpp:67-72): the per-all-reduce payload."""
+        self.validate()
+        return self.batch_size * self.hidden_dim * self.bytes_per_element
+
+    def allreduces_per_step(self) -> int:
+        """Two per layer (attention and MLP output projections)."""
+        return 2 * self.num_layers
+
+
+class TpDecodeSkeleton:
+    """One rank's share of a Llama decode step (see the module docstring)."""
+
+    def __init__(self, model: str, batch: int, tp: int, device: torch.device,
+                 weight_sets: int = 2, seed: int = 0, layers: int | None = None):
+        cfg = LLAMA[model]
+        h, ffn = cfg["hidden"], cfg["ffn"]
+        hd = h // cfg["heads"]
+        if cfg["heads"] % tp or cfg["kv_heads"] % tp or ffn % tp:
+            raise ValueError(f"TP={tp} does not divide the {model} heads / ffn")
+        self.hidden, self.tp, self.batch = h, tp, batch
+        self.layers = layers or cfg["layers"]
+        qkv = (cfg["heads"] + 2 * cfg["kv_heads"]) * hd // tp
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+
+        def w(r, c):
+            return (torch.randn(r, c, device=device, generator=g, dtype=torch.float32)
+                    * (r ** -0.5)).to(torch.bfloat16)
+
+        self.sets = [dict(qkv=w(h, qkv), o=w(h // tp, h), gu=w(h, 2 * ffn // tp),
+                          down=w(ffn // tp, h)) for _ in range(weight_sets)]
+        self.x0 = (torch.randn(batch, h, device=device, generator=g) * 0.1).to(torch.bfloat16)
+        self.x = self.x0.clone()
+        self.ffn_shard = ffn // tp
+
+    def weight_bytes_per_layer(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.sets[0].values())
+
+    def step(self, all_reduce) -> None:
+        """One decode step over all layers; all_reduce(t) sums t in place over ranks
+        (None = skip the collective, for the compute-only reference)."""
+        x = self.x
+        x.copy_(self.x0)
+        hs = self.hidden // self.tp
+        for layer in range(self.layers):
+            W = self.sets[layer % len(self.sets)]
+            qkv = F.rms_norm(x, (self.hidden,)) @ W["qkv"]
+            a = qkv[:, :hs] @ W["o"]
+            if all_reduce is not None:
+                all_reduce(a)
+            x = x + a
+            gu = F.rms_norm(x, (self.hidden,)) @ W["gu"]
+            d = (F.silu(gu[:, :self.ffn_shard]) * gu[:, self.ffn_shard:]) @ W["down"]
+            if all_reduce is not None:
+                all_reduce(d)
+            x = x + d
+        self.out = x
+
+
+def _graph(fn, warmup: int = 2) -> torch.cuda.CUDAGraph:
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(warmup):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        fn()
+    torch.cuda.synchronize()
+    return gr
+
+
+def _time(gr: torch.cuda.CUDAGraph, iters: int, warmup: int) -> list:
+    import torch.distributed as dist
+    out = []
+    for i in range(warmup + iters):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        gr.replay()
+        b.record()
+        b.synchronize()
+        if i >= warmup:
+            t = torch.tensor([a.elapsed_time(b)], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            out.append(float(t.item()))
+    return out
+
+
+def main() -> None:
+    import torch.distributed as dist
+
+    from . import torch_op
+    from .comm import ClusterTopology, Communicator
+    from .selector import autotune
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="70b", choices=sorted(LLAMA))
+    ap.add_argument("--batch", default="8,16,32,64,128")
+    ap.add_argument("--layers", type=int, default=0, help="0 = the model's layer count")
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--no-autotune", action="store_true")
+    args = ap.parse_args()
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, tp = dist.get_rank(), dist.get_world_size()
+    cfg = LLAMA[args.model]
+    batches = [int(b) for b in args.batch.split(",")]
+    max_bytes = max(batches) * cfg["hidden"] * 2
+    nodes = 2 if tp >= 2 else 1
+    topo = ClusterTopology(nodes, tp // nodes)
+    comm = Communicator.from_process_group(topo, max_bytes, device=local)
+    if not args.no_autotune:
+        autotune(comm, [b * cfg["hidden"] * 2 for b in batches], dtype=torch.bfloat16)
+    cid = torch_op.register(comm)
+
+    def nvrar_ar(t):
+        torch.ops.nvrar.all_reduce_(t, cid)
+
+    def nccl_ar(t):
+        dist.all_reduce(t)
+
+    for batch in batches:
+        wl = DecodeWorkload(batch, cfg["hidden"], 2, args.layers or cfg["layers"])
+        m = TpDecodeSkeleton(args.model, batch, tp, torch.device("cuda", local),
+                             layers=args.layers or None)
+        res = {}
+        outs = {}
+        for name, ar in (("nvrar", nvrar_ar), ("nccl", nccl_ar), ("compute_only", None)):
+            gr = _graph(lambda: m.step(ar))
+            ts = _time(gr, args.iters, args.warmup)
+            res[name] = statistics.median(ts)
+            outs[name] = m.out.float().clone()
+            del gr
+        comm.check()
+        # both collectives must give the same model output (bf16 sums, different orders)
+        diff = float((outs["nvrar"] - outs["nccl"]).abs().max())
+        scale = float(outs["nccl"].abs().max())
+        if rank == 0:
+            comm_nv = res["nvrar"] - res["compute_only"]
+            comm_nc = res["nccl"] - res["compute_only"]
+            print(json.dumps({
+                "model": f"llama-3.1-{args.model}", "tp": tp, "batch": batch,
+                "msg_bytes": wl.msg_bytes(), "allreduces_per_step": wl.allreduces_per_step(),
+                "step_ms": {k: round(v, 4) for k, v in res.items()},
+                "comm_ms": {"nvrar": round(comm_nv, 4), "nccl": round(comm_nc, 4)},
+                "per_allreduce_us": {"nvrar": round(comm_nv * 1e3 / wl.allreduces_per_step(), 3),
+                                     "nccl": round(comm_nc * 1e3 / wl.allreduces_per_step(), 3)},
+                "step_speedup_vs_nccl": round(res["nccl"] / res["nvrar"], 4),
+                "weight_mb_per_layer": round(m.weight_bytes_per_layer() / 2**20, 1),
+                "max_abs_diff_vs_nccl": diff, "out_scale": scale,
+                "timing": "CUDA graph of one full step, CUDA events, max over ranks, median",
+            }), flush=True)
+        del m
+        torch.cuda.empty_cache()
+    torch_op.unregister(cid)
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
