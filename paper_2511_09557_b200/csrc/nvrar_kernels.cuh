@@ -721,6 +721,8 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   constexpr int RDW = 4;
   constexpr int kLevels = Log2<N>::value + 1;
   const RankDesc& d = *lp.desc[blockIdx.y];
+  // the descriptor is immutable while calls run: read it before the wait
+  RankState* const st = d.state;
   begin_wait(d);
   const uint32_t n = static_cast<uint32_t>(lp.count);
   const int G = lp.d0.gpus, P = lp.nlocal;  // param space: no dependent load
@@ -754,10 +756,7 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
     }
   };
   uint32_t u = ub + threadIdx.x;
-  // the first unit's loads do not depend on the call number: issue them first
   if (u < ue) load_unit(u);
-  Ctl c;
-  if (!begin_seq(d, c)) return;
   while (u < ue) {
     const uint32_t e0 = UE * u;
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
@@ -815,7 +814,16 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
     if (u < ue) load_unit(u);
     for (int r2 = 0; r2 < P; ++r2) store_raw<E, UE>(lp.recv[r2], e0, valid, o);
   }
-  end_call(d, c.seq);
+  // Nothing here waits on a peer, so the call number is never needed: advance
+  // this CTA's replicated counter slots by one without reading them (a sticky
+  // fault cannot arise in this schedule; the host refuses a failed comm).
+  if (threadIdx.x < 32) {
+    for (int i = blockIdx.x + static_cast<int>(threadIdx.x) * gridDim.x; i < kSeqSlots;
+         i += 32 * gridDim.x) {
+      atomicAdd(&st->seq[i], 1u);
+    }
+  }
+  stamp(d, 6);
 }
 
 using KernelFn = void (*)(LaunchParams);
