@@ -12,7 +12,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB_DIR = os.path.join(PKG, "lib")
+LIB_DIR = os.environ.get("NVRAR_BUILD_DIR") or os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libnvrar_b200.so")
 SOURCES = ["nvrar_inst_f32.cu", "nvrar_inst_bf16.cu", "nvrar_inst_i32.cu",
            "nvrar_inst_phase_f.cu", "nvrar_inst_phase_i.cu", "nvrar_misc.cu", "nvrar_comm.cu"]
@@ -22,6 +22,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--fmad=false", "-cudart", "static", "-I" + os.path.join(ROOT, "include")]
+# experiments only: extra nvcc flags (e.g. -DNVRAR_PUT_ST=...) and an output
+# directory other than the in-tree lib/ (the product build uses neither)
+EXTRA = os.environ.get("NVRAR_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:
@@ -43,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(LIB_DIR, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

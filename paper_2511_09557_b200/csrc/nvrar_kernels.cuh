@@ -548,6 +548,9 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       Raw::template put<RDW>(slot, u, raw, c.seq);
     }
   }
+#ifdef NVRAR_PUSH_FENCE
+  __threadfence_system();  // experiment: push the remote stores out now
+#endif
   stamp(d, 2);
   c.phase = 3;
 

@@ -37,7 +37,8 @@ __device__ __forceinline__ uint64_t gt() {
 }
 
 __global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint64_t* stamps,
-                     int sleep_ns, int leader) {
+                     int sleep_ns, int leader, int bulk) {
+  extern __shared__ uint4 stage[];
   // start barrier across GPUs so launch skew does not count
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) pr.ready[me] = val;
@@ -52,6 +53,24 @@ __global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint
     stamps[3 * blockIdx.x] = gt();
   }
   __syncthreads();
+  if (bulk) {
+    // TMA bulk copy: this CTA's contiguous range, staged once in shared memory,
+    // one cp.async.bulk per peer (large NVLink writes instead of 16-byte stores)
+    const uint64_t c0 = cells * blockIdx.x / gridDim.x, c1 = cells * (blockIdx.x + 1) / gridDim.x;
+    for (uint64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) stage[i - c0] = make_uint4(val, val, val, val);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0 && c1 > c0) {
+      const uint32_t sm = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+      for (int j = 1; j < P; ++j) {
+        const int q = (me + j) % P;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(pr.slot[q] + c0),
+                     "r"(sm), "r"(static_cast<uint32_t>((c1 - c0) * 16)) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+  } else {
   for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cells;
        i += (uint64_t)gridDim.x * blockDim.x) {
     for (int j = 1; j < P; ++j) {
@@ -59,6 +78,7 @@ __global__ void exch(Peers pr, int me, int P, uint64_t cells, uint32_t val, uint
       asm volatile("st.volatile.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(pr.slot[q] + i),
                    "r"(val));
     }
+  }
   }
   if (threadIdx.x == 0) stamps[3 * blockIdx.x + 1] = gt();
   for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cells;
@@ -162,13 +182,20 @@ int main() {
   }
   printf("P=%d\n", P);
   uint32_t val = 0x40000000u;
-  for (int variant = 0; variant < 5; ++variant) {
+  for (int g = 0; g < P; ++g) {
+    CK(cudaSetDevice(g));
+    CK(cudaFuncSetAttribute(exch, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10));
+  }
+  for (int variant = 1; variant < 6; variant += 4) {
   const int sleep_ns = variant == 0 ? 0 : variant == 1 ? 32 : variant == 2 ? 256 : variant == 3 ? 1000 : 32;
   const int leader = variant == 4;
-  printf("-- poll sleep %d ns%s\n", sleep_ns, leader ? ", warp-leader poll" : "");
-  for (uint64_t bytes : {16ull << 10, 128ull << 10, 512ull << 10, 2048ull << 10}) {
+  const int bulk = variant == 5;
+  printf("-- poll sleep %d ns%s%s\n", sleep_ns, leader ? ", warp-leader poll" : "",
+         bulk ? ", TMA bulk pushes" : "");
+  for (uint64_t bytes : {16ull, 512ull, 4ull << 10, 16ull << 10, 128ull << 10, 512ull << 10,
+                         2048ull << 10}) {
     for (int grid : {32, 128}) {
-      std::vector<double> tot, iss;
+      std::vector<double> tot, iss, lat;
       for (int rep = 0; rep < 5; ++rep) {
         ++val;
         for (int g = 0; g < P; ++g) {
@@ -185,9 +212,10 @@ int main() {
           pr.ready = ready;
           for (int q = 0; q < P; ++q) pr.go[q] = gow[q];
           CK(cudaSetDevice(g));
-          exch<<<grid, 512, 0, s[g]>>>(pr, g, P, bytes / 16, val, st[g], sleep_ns, leader);
+          const size_t smem = bulk ? ((bytes / 16 + grid - 1) / grid) * 16 : 0;
+          exch<<<grid, 512, smem, s[g]>>>(pr, g, P, bytes / 16, val, st[g], sleep_ns, leader && !bulk, bulk);
         }
-        double t0 = 1e30, t_end = 0, iss_end = 0;
+        double t0 = 1e30, t_end = 0, iss_end = 0, t0_last = 0;
         for (int g = 0; g < P; ++g) {
           CK(cudaSetDevice(g));
           CK(cudaStreamSynchronize(s[g]));
@@ -195,17 +223,21 @@ int main() {
           CK(cudaMemcpy(h.data(), st[g], 24 * grid, cudaMemcpyDeviceToHost));
           for (int b = 0; b < grid; ++b) {
             t0 = std::min(t0, (double)h[3 * b] - off[g]);
+            t0_last = std::max(t0_last, (double)h[3 * b] - off[g]);
             iss_end = std::max(iss_end, (double)h[3 * b + 1] - off[g]);
             t_end = std::max(t_end, (double)h[3 * b + 2] - off[g]);
           }
         }
         tot.push_back((t_end - t0) / 1e3);
         iss.push_back((iss_end - t0) / 1e3);
+        lat.push_back((t_end - t0_last) / 1e3);
       }
       std::sort(tot.begin(), tot.end());
       std::sort(iss.begin(), iss.end());
-      printf("bytes/peer=%8llu grid=%4d : pushes issued by %.3f us, all arrived by %.3f us (p50)\n",
-             (unsigned long long)bytes, grid, iss[2], tot[2]);
+      std::sort(lat.begin(), lat.end());
+      printf("bytes/peer=%8llu grid=%4d : pushes issued by %.3f us, all arrived by %.3f us, "
+             "last start -> last arrival %.3f us (p50)\n",
+             (unsigned long long)bytes, grid, iss[2], tot[2], lat[2]);
     }
   }
   }
