@@ -11,7 +11,7 @@ import os
 
 from . import build as _build
 
-LIB_PATH = os.environ.get("NVRAR_LIB", _build.LIB)  # override: experiment builds
+LIB_PATH = os.environ.get("NVRAR_LIB") or _build.LIB  # override: experiment builds
 
 SUCCESS = 0
 ERR_INTERNAL = 1

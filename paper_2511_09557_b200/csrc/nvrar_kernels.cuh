@@ -76,13 +76,30 @@ __device__ __forceinline__ void begin_wait(const RankDesc& d) {
   stamp(d, 7);
 }
 
+#ifndef NVRAR_SEQ_LD
+#define NVRAR_SEQ_LD "ld.volatile.global.u32"
+#endif
+// The call number and the sticky fault word of this CTA (thread 0 only). Only
+// this GPU's kernels write them.
+struct SeqWords {
+  uint32_t err, seq;
+};
+__device__ __forceinline__ SeqWords seq_issue(const RankDesc& d) {
+  SeqWords w{0u, 0u};
+  if (threadIdx.x == 0) {
+    asm volatile(NVRAR_SEQ_LD " %0, [%1];" : "=r"(w.err) : "l"(&d.state->err.code));
+    asm volatile(NVRAR_SEQ_LD " %0, [%1];" : "=r"(w.seq) : "l"(&d.state->seq[blockIdx.x]));
+  }
+  return w;
+}
+
 // Prologue, part 2 (after the caller has issued its first input loads, which
 // do not depend on the call number). Returns false on a sticky fault.
-__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
+__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, SeqWords w) {
   __shared__ uint32_t s_seq, s_err;
   if (threadIdx.x == 0) {
-    s_err = ld_volatile32(&d.state->err.code);
-    s_seq = ld_volatile32(&d.state->seq[blockIdx.x]);
+    s_err = w.err;
+    s_seq = w.seq;
   }
   __syncthreads();
   c.st = d.state;
@@ -96,6 +113,9 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
   c.phase = 2;
   stamp(d, 1);
   return s_err == 0u;
+}
+__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
+  return begin_seq(d, c, seq_issue(d));
 }
 
 __device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
@@ -207,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   for (int j = 0; j < kHierMaxG; ++j) grp[j] = local + j >= G ? local + j - G : local + j;
 
   begin_wait(d);
-  // Prefetch this thread's first unit of every chunk before the call number is
+  const SeqWords sw = seq_issue(d);
+  // Prefetch this thread's first unit of every chunk while the call number is
   // read (the loads do not depend on it): pre[j] = chunk (local + j) % G.
   uint32_t pre[kHierMaxG][RDW];
   int pv[kHierMaxG];
@@ -221,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
   }
   Ctl c;
-  if (!begin_seq(d, c)) return;  // sticky fault: comm is dead
+  if (!begin_seq(d, c, sw)) return;  // sticky fault: comm is dead
   const uint32_t parity = c.seq & 1u;
 
   // Peer-only sync, publish half (nvrar.hpp:163-171).
@@ -499,6 +520,8 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const uint64_t u_first = ub + threadIdx.x;
 
   begin_wait(d);
+  // the call-number load first: its latency overlaps the input prefetch
+  const SeqWords sw = seq_issue(d);
   // Prefetch this thread's first unit of every sub-shard (pre[j]: owner
   // (me + j) % P; j = 0 is our own) before the call number is read. One-shot
   // sends the same unit to everyone, so it loads once.
@@ -515,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
   }
   Ctl c;
-  if (!begin_seq(d, c)) return;
+  if (!begin_seq(d, c, sw)) return;
   const uint32_t parity = c.seq & 1u;
 
   if (blockIdx.x == 0) {
