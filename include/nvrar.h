@@ -171,6 +171,31 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
                           void* const* recv, size_t count, nvrar_dtype_t dtype, nvrar_op_t op,
                           void* stream, uint64_t active_mask);
 
+/* ---- the reference's baseline collectives --------------------------------
+ * The same sum with the reduction ORDER of the reference's other two
+ * all-reduces, for model validation against them (they run on the flat
+ * schedules; NCCL remains the performance baseline):
+ *   RING — RingAllreduce<T> (ring.hpp): ring fold over all P ranks in ring
+ *          positions p -> rank (p mod N, p div N), chunk = ceil(n/P);
+ *          P <= 8.
+ *   TREE — TreeAllreduce<T> (tree.hpp:10-12): in[0] + (in[1] + (... + in[G-1]))
+ *          per node, then the pairwise tree over nodes.
+ * Bit-exact to tests/oracles.hpp ring_order_sum / tree_order_sum. */
+typedef enum {
+  NVRAR_ORDER_NVRAR = 0,
+  NVRAR_ORDER_RING = 1,
+  NVRAR_ORDER_TREE = 2
+} nvrar_order_t;
+int nvrar_ring_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
+int nvrar_tree_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
+/* nvrar_allreduce_local with an explicit nvrar_order_t. */
+int nvrar_allreduce_local_order(nvrar_comm_t* comms, int ncomms, int order,
+                                const void* const* send, void* const* recv, size_t count,
+                                nvrar_dtype_t dtype, nvrar_op_t op, void* stream,
+                                uint64_t active_mask);
+
 /* ---- phase-only entry points --------------------------------------------
  * One phase of the hierarchical all-reduce on its own, run by the same kernel
  * code as nvrar_allreduce (debugging and phase-level parity). Each call

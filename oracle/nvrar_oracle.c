@@ -179,6 +179,56 @@ DEFINE_ORDER_SUM(orc_nvrar_order_sum_i32, int32_t, add_i32)
     return 0;                                                                       \
   }
 
+/* ring_order_sum (tests/oracles.hpp:67-86): ring positions p -> rank
+ * (p mod N, p div N); ce = ceil(n/P); element e in chunk c = e / ce is the ring
+ * fold by position: x[(c+1)%P] + ... + x[c] (ring_chunk_fold, :45-58).
+ * tree_order_sum (:137-159): per node t = in[G-1]; t = in[lr] + t for
+ * lr = G-2..0; then for bit = 1,2,..: t[node] += t[node+bit] (node % 2bit == 0). */
+#define DEFINE_RING_ORDER(NAME, T, ADD)                                             \
+  int NAME(int nodes, int gpus, size_t n, const T* inputs, T* out) {                \
+    if (nodes < 1 || gpus < 1) return -2;                                           \
+    const int p = nodes * gpus;                                                     \
+    if (n == 0) return 0;                                                           \
+    const size_t ce = (n + (size_t)p - 1) / (size_t)p;                              \
+    for (size_t e = 0; e < n; ++e) {                                                \
+      const int c = (int)(e / ce);                                                  \
+      T f = (T)0;                                                                   \
+      for (int j = 1; j <= p; ++j) {                                                \
+        const int pos = (c + j) % p;                                                \
+        const int rank = (pos % nodes) * gpus + pos / nodes;                        \
+        const T x = inputs[(size_t)rank * n + e];                                   \
+        f = j == 1 ? x : ADD(f, x);                                                 \
+      }                                                                             \
+      out[e] = f;                                                                   \
+    }                                                                               \
+    return 0;                                                                       \
+  }
+
+#define DEFINE_TREE_ORDER(NAME, T, ADD)                                             \
+  int NAME(int nodes, int gpus, size_t n, const T* inputs, T* out) {                \
+    if (nodes < 1 || gpus < 1) return -2;                                           \
+    if (!is_pow2(nodes) || nodes > ORC_MAX_NODES) return -1;                        \
+    T t[ORC_MAX_NODES];                                                             \
+    for (size_t e = 0; e < n; ++e) {                                                \
+      for (int node = 0; node < nodes; ++node) {                                    \
+        const T* base = inputs + (size_t)node * (size_t)gpus * n;                   \
+        T v = base[(size_t)(gpus - 1) * n + e];                                     \
+        for (int lr = gpus - 2; lr >= 0; --lr) v = ADD(base[(size_t)lr * n + e], v);  \
+        t[node] = v;                                                                \
+      }                                                                             \
+      for (int bit = 1; bit < nodes; bit <<= 1) {                                   \
+        for (int node = 0; node < nodes; node += 2 * bit) t[node] = ADD(t[node], t[node + bit]); \
+      }                                                                             \
+      out[e] = t[0];                                                                \
+    }                                                                               \
+    return 0;                                                                       \
+  }
+
+DEFINE_RING_ORDER(orc_ring_order_sum_f32, float, add_f32)
+DEFINE_RING_ORDER(orc_ring_order_sum_i32, int32_t, add_i32)
+DEFINE_TREE_ORDER(orc_tree_order_sum_f32, float, add_f32)
+DEFINE_TREE_ORDER(orc_tree_order_sum_i32, int32_t, add_i32)
+
 DEFINE_INTRA_RS(orc_intra_rs_sum_f32, float, add_f32)
 DEFINE_INTRA_RS(orc_intra_rs_sum_i32, int32_t, add_i32)
 DEFINE_RD_INTER(orc_rd_inter_f32, float, add_f32)

@@ -59,6 +59,13 @@ int orc_nvrar_order_sum_bf16(int nodes, int gpus, size_t n, const uint16_t* inpu
                              uint16_t* out);
 
 /* oracles::serial_sum: global-rank order. */
+/* The reference's baseline collectives' orders: ring_order_sum
+ * (tests/oracles.hpp:67-86) and tree_order_sum (:137-159). */
+int orc_ring_order_sum_f32(int nodes, int gpus, size_t n, const float* inputs, float* out);
+int orc_ring_order_sum_i32(int nodes, int gpus, size_t n, const int32_t* inputs, int32_t* out);
+int orc_tree_order_sum_f32(int nodes, int gpus, size_t n, const float* inputs, float* out);
+int orc_tree_order_sum_i32(int nodes, int gpus, size_t n, const int32_t* inputs, int32_t* out);
+
 /* Standalone phases: intra_rs_sum (tests/oracles.hpp:89-97; out = ce*G
  * elements) and the rd_inter result (nvrar.hpp:132-155; P x w rank-major). */
 int orc_intra_rs_sum_f32(int gpus, size_t n, const float* inputs, float* out);

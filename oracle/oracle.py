@@ -54,6 +54,10 @@ def lib():
                      "orc_nvrar_order_sum_bf16"):
             getattr(L, name).argtypes = [ctypes.c_int, ctypes.c_int, c_sz, vp, vp]
             getattr(L, name).restype = ctypes.c_int
+        for name in ("orc_ring_order_sum_f32", "orc_ring_order_sum_i32",
+                     "orc_tree_order_sum_f32", "orc_tree_order_sum_i32"):
+            getattr(L, name).argtypes = [ctypes.c_int, ctypes.c_int, c_sz, vp, vp]
+            getattr(L, name).restype = ctypes.c_int
         for name in ("orc_intra_rs_sum_f32", "orc_intra_rs_sum_i32"):
             getattr(L, name).argtypes = [ctypes.c_int, c_sz, vp, vp]
             getattr(L, name).restype = ctypes.c_int
@@ -100,6 +104,10 @@ def ref():
         R.ref_nvrar_stalled_rank.restype = ci
         for name in ("ref_intra_rs_f32", "ref_intra_rs_i32", "ref_intra_ag_f32",
                      "ref_intra_ag_i32"):
+            getattr(R, name).argtypes = [ci, ci, c_sz, vp, vp, ctypes.c_char_p, c_sz]
+            getattr(R, name).restype = ci
+        for name in ("ref_ring_run_all_f32", "ref_ring_run_all_i32", "ref_tree_run_all_f32",
+                     "ref_tree_run_all_i32"):
             getattr(R, name).argtypes = [ci, ci, c_sz, vp, vp, ctypes.c_char_p, c_sz]
             getattr(R, name).restype = ci
         for name in ("ref_rd_inter_f32", "ref_rd_inter_i32"):
@@ -156,6 +164,30 @@ def nvrar_order_sum(inputs: np.ndarray, nodes: int, gpus: int, dtype: str = "f32
     inputs = inputs.astype(fn[1], copy=False)
     out = np.empty(n, fn[1])
     rc = getattr(lib(), fn[0])(nodes, gpus, n, _ptr(inputs), _ptr(out))
+    if rc == -1:
+        raise ValueError(f"nodes={nodes} is not a power of two")
+    if rc != 0:
+        raise RuntimeError(f"oracle rc={rc}")
+    return out
+
+
+def order_sum(inputs: np.ndarray, nodes: int, gpus: int, order: str = "nvrar",
+              dtype: str = "f32") -> np.ndarray:
+    """The result bits of the reference's three all-reduces for hierarchy
+    nodes x gpus: 'nvrar' (oracles.hpp:101-133), 'ring' (ring_order_sum,
+    :67-86), 'tree' (tree_order_sum, :137-159). bf16 = the fp32 order sum of
+    the up-cast inputs, one RNE rounding."""
+    if order == "nvrar":
+        return nvrar_order_sum(inputs, nodes, gpus, dtype)
+    x = np.ascontiguousarray(inputs)
+    if dtype == "bf16":
+        return bf16_bits_from_f32(order_sum(f32_from_bf16_bits(x), nodes, gpus, order, "f32"))
+    p, n = x.shape
+    assert p == nodes * gpus
+    suffix = "f32" if dtype == "f32" else "i32"
+    x = x.astype(np.float32 if suffix == "f32" else np.int32, copy=False)
+    out = np.empty(n, x.dtype)
+    rc = getattr(lib(), f"orc_{order}_order_sum_{suffix}")(nodes, gpus, n, _ptr(x), _ptr(out))
     if rc == -1:
         raise ValueError(f"nodes={nodes} is not a power of two")
     if rc != 0:
@@ -303,6 +335,19 @@ def ref_intra_phase(which: str, inputs: np.ndarray, nodes: int, gpus: int) -> np
     suffix = "f32" if x.dtype == np.float32 else "i32"
     err = ctypes.create_string_buffer(512)
     rc = getattr(ref(), f"ref_intra_{which}_{suffix}")(nodes, gpus, ln, _ptr(x), _ptr(out), err, 512)
+    if rc != 0:
+        raise RefError(rc, err.value.decode())
+    return out
+
+
+def ref_baseline_run_all(which: str, inputs: np.ndarray, nodes: int, gpus: int) -> np.ndarray:
+    """Every rank runs ccsim::RingAllreduce<T> ('ring') or TreeAllreduce<T> ('tree')."""
+    x = np.ascontiguousarray(inputs)
+    out = np.empty_like(x)
+    suffix = "f32" if x.dtype == np.float32 else "i32"
+    err = ctypes.create_string_buffer(512)
+    rc = getattr(ref(), f"ref_{which}_run_all_{suffix}")(nodes, gpus, x.shape[1], _ptr(x),
+                                                          _ptr(out), err, 512)
     if rc != 0:
         raise RefError(rc, err.value.decode())
     return out

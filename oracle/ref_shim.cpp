@@ -154,6 +154,33 @@ int rd_inter_all(int nodes, int gpus, std::size_t w, const T* shards, T* outputs
   });
 }
 
+// RingAllreduce<T> / TreeAllreduce<T> (ring.hpp, tree.hpp) on every rank.
+template <Element T>
+int baseline_all(int which, int nodes, int gpus, std::size_t n, const T* inputs, T* outputs,
+                 char* err, std::size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const ClusterTopology topo{nodes, gpus};
+    topo.validate();
+    const int ng = topo.world_size();
+    auto in = unflatten(inputs, ng, n);
+    std::vector<std::vector<T>> out(ng, std::vector<T>(n));
+    auto program = [&](Ctx& ctx) -> Task {
+      const int me = ctx.global();
+      if (which == 0) {
+        RingAllreduce<T> coll(ctx, n);
+        co_await coll.run(std::span<const T>(in[me]), std::span<T>(out[me]));
+      } else {
+        TreeAllreduce<T> coll(ctx, n);
+        co_await coll.run(std::span<const T>(in[me]), std::span<T>(out[me]));
+      }
+    };
+    run_ranks(topo, CostParams{}, TransportMode::VirtualTime, {}, program);
+    for (int r = 0; r < ng; ++r) {
+      std::memcpy(outputs + static_cast<std::size_t>(r) * n, out[r].data(), n * sizeof(T));
+    }
+  });
+}
+
 // Times NvrarAllreduce<T>::run on ConcurrentEngine with pre-generated inputs
 // (unlike run_bench_point, which generates inputs inside its timed loop,
 // bench.hpp:92-93). Per call: makespan = max over ranks of the wall time at
@@ -243,6 +270,23 @@ int ref_nvrar_run_all_i32(int nodes, int gpus, std::size_t n, const std::int32_t
                           std::size_t errlen) {
   return run_all<std::int32_t>(nodes, gpus, n, inputs, outputs, blocks, chunk, mode, seed,
                                delay_us, timeout_s, err, errlen);
+}
+
+int ref_ring_run_all_f32(int nodes, int gpus, std::size_t n, const float* in, float* out,
+                         char* err, std::size_t errlen) {
+  return baseline_all<float>(0, nodes, gpus, n, in, out, err, errlen);
+}
+int ref_ring_run_all_i32(int nodes, int gpus, std::size_t n, const std::int32_t* in,
+                         std::int32_t* out, char* err, std::size_t errlen) {
+  return baseline_all<std::int32_t>(0, nodes, gpus, n, in, out, err, errlen);
+}
+int ref_tree_run_all_f32(int nodes, int gpus, std::size_t n, const float* in, float* out,
+                         char* err, std::size_t errlen) {
+  return baseline_all<float>(1, nodes, gpus, n, in, out, err, errlen);
+}
+int ref_tree_run_all_i32(int nodes, int gpus, std::size_t n, const std::int32_t* in,
+                         std::int32_t* out, char* err, std::size_t errlen) {
+  return baseline_all<std::int32_t>(1, nodes, gpus, n, in, out, err, errlen);
 }
 
 int ref_intra_rs_f32(int nodes, int gpus, std::size_t n, const float* in, float* out, char* err,

@@ -309,6 +309,23 @@ class Communicator:
         if rc:
             _raise(rc, self.last_error(), self.rank)
 
+    # ---- the reference's baseline collectives (ring.hpp / tree.hpp orders) ----
+    def ring_allreduce(self, send: torch.Tensor, recv: torch.Tensor,
+                       stream: Optional[torch.cuda.Stream] = None) -> None:
+        """RingAllreduce<T>::run's result bits (ring_order_sum)."""
+        _check_pair(send, recv)
+        self._check(self._lib.nvrar_ring_allreduce(self._h, send.data_ptr(), recv.data_ptr(),
+                                                   send.numel(), dtype_code(send.dtype), L.SUM,
+                                                   _stream_ptr(stream)))
+
+    def tree_allreduce(self, send: torch.Tensor, recv: torch.Tensor,
+                       stream: Optional[torch.cuda.Stream] = None) -> None:
+        """TreeAllreduce<T>::run's result bits (tree_order_sum)."""
+        _check_pair(send, recv)
+        self._check(self._lib.nvrar_tree_allreduce(self._h, send.data_ptr(), recv.data_ptr(),
+                                                   send.numel(), dtype_code(send.dtype), L.SUM,
+                                                   _stream_ptr(stream)))
+
     # ---- phase-only entry points (nvrar.h "phase-only entry points") ----------
     def reduce_scatter(self, send: torch.Tensor, shard: torch.Tensor,
                        stream: Optional[torch.cuda.Stream] = None) -> None:
@@ -378,6 +395,8 @@ def _check_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
 
 
 PHASE_REDUCE_SCATTER, PHASE_RD_INTER, PHASE_ALL_GATHER = 1, 2, 3
+# reduction orders of the reference's three all-reduces (nvrar.h nvrar_order_t)
+_ORDERS = {"nvrar": 0, "ring": 1, "tree": 2}
 _PHASES = {"reduce_scatter": PHASE_REDUCE_SCATTER, "rd_inter": PHASE_RD_INTER,
            "all_gather": PHASE_ALL_GATHER}
 
@@ -483,7 +502,7 @@ class LocalGroup:
 
     def launch(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
                active: Optional[Sequence[int]] = None,
-               stream: Optional[torch.cuda.Stream] = None) -> None:
+               stream: Optional[torch.cuda.Stream] = None, order: str = "nvrar") -> None:
         p = self.topo.world_size()
         if len(inputs) != p or len(outputs) != p:
             raise InvalidArgumentError("one input and one output per rank")
@@ -494,8 +513,12 @@ class LocalGroup:
         send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
         recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])
         mask = (1 << 64) - 1 if active is None else sum(1 << r for r in active)
-        rc = self._lib.nvrar_allreduce_local(self._arr, p, send, recv, n, dt, L.SUM,
-                                             _stream_ptr(stream), mask)
+        if order == "nvrar":
+            rc = self._lib.nvrar_allreduce_local(self._arr, p, send, recv, n, dt, L.SUM,
+                                                 _stream_ptr(stream), mask)
+        else:
+            rc = self._lib.nvrar_allreduce_local_order(self._arr, p, _ORDERS[order], send, recv,
+                                                       n, dt, L.SUM, _stream_ptr(stream), mask)
         if rc:
             _raise(rc, self.comms[0].last_error())
 
@@ -543,10 +566,10 @@ class LocalGroup:
 
     def run_all(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
                 cfg: Optional[NvrarConfig] = None, active: Optional[Sequence[int]] = None,
-                check: bool = True) -> None:
+                check: bool = True, order: str = "nvrar") -> None:
         if cfg is not None:
             self.set_config(cfg)
-        self.launch(inputs, outputs, active)
+        self.launch(inputs, outputs, active, order=order)
         if check:
             self.check()
 

@@ -622,9 +622,22 @@ static size_t phase_bytes(const nvrar_comm* c, int phase, size_t count, int dtyp
 
 static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void* const* recv,
                   size_t count, int dtype, int op, void* stream, uint64_t mask, bool local_group,
-                  int phase = NVRAR_PHASE_ALL) {
+                  int phase = NVRAR_PHASE_ALL, int order = NVRAR_ORDER_NVRAR) {
   nvrar_comm* c0 = comms[0];
   if (op != NVRAR_SUM) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "only SUM is supported");
+  if (order < NVRAR_ORDER_NVRAR || order > NVRAR_ORDER_TREE) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "bad reduction order %d", order);
+  }
+  // ring / tree orders run on the flat kernel: its register tile bounds them
+  if (order == NVRAR_ORDER_RING && c0->world > flat_max_gpus(1)) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "ring order: at most %d ranks",
+                flat_max_gpus(1));
+  }
+  if (order == NVRAR_ORDER_TREE &&
+      (c0->gpus > flat_max_gpus(c0->nodes) || c0->world > 16)) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "tree order: unsupported topology %dx%d",
+                c0->nodes, c0->gpus);
+  }
   if (dtype < NVRAR_INT32 || dtype > NVRAR_BF16) {
     return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
   }
@@ -683,6 +696,21 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
     algo = NVRAR_ALGO_HIER;
     if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   }
+  if (order != NVRAR_ORDER_NVRAR && algo != NVRAR_ALGO_ONESHOT && algo != NVRAR_ALGO_TWOSHOT) {
+    // the ring / tree orders exist on the flat schedules only
+    algo = count * dtype_bytes(dtype) <= (c0->world <= 4 ? (1u << 20) : (256u << 10)) &&
+                   count * dtype_bytes(dtype) <= kOneshotMaxBytes
+               ? NVRAR_ALGO_ONESHOT
+               : NVRAR_ALGO_TWOSHOT;
+    if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  }
+  lp.order = order;
+  if (order == NVRAR_ORDER_RING) {
+    // ring positions are local-rank-major: position p -> rank (p mod N, p div N)
+    for (int p = 0; p < c0->world; ++p) {
+      lp.perm[p] = static_cast<uint8_t>((p % c0->nodes) * c0->gpus + p / c0->nodes);
+    }
+  }
   const bool direct = algo == NVRAR_ALGO_DIRECT;
   lp.oneshot = algo == NVRAR_ALGO_ONESHOT;
   // by value: the kernel reads it from param space (EMU: only the topology fields
@@ -691,7 +719,8 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
   KernelFn k = phase != NVRAR_PHASE_ALL ? select_phase(dtype, phase, c0->nodes, emu)
                : direct ? select_direct(dtype, c0->nodes)
-                        : select_kernel(dtype, algo != NVRAR_ALGO_HIER, c0->nodes, emu, lamport);
+                        : select_kernel(dtype, algo != NVRAR_ALGO_HIER,
+                                        order == NVRAR_ORDER_RING ? 1 : c0->nodes, emu, lamport);
   if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
 
   cudaLaunchConfig_t cfg{};
@@ -724,6 +753,35 @@ int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t coun
   const void* s[1] = {send};
   void* r[1] = {recv};
   return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false);
+}
+
+int nvrar_ring_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  const void* s[1] = {send};
+  void* r[1] = {recv};
+  return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false, NVRAR_PHASE_ALL,
+                NVRAR_ORDER_RING);
+}
+
+int nvrar_tree_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  const void* s[1] = {send};
+  void* r[1] = {recv};
+  return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false, NVRAR_PHASE_ALL,
+                NVRAR_ORDER_TREE);
+}
+
+int nvrar_allreduce_local_order(nvrar_comm_t* comms, int ncomms, int order,
+                                const void* const* send, void* const* recv, size_t count,
+                                nvrar_dtype_t dtype, nvrar_op_t op, void* stream,
+                                uint64_t active_mask) {
+  if (!comms || ncomms < 1 || ncomms > NVRAR_MAX_LOCAL || !send || !recv) {
+    return fail(comms ? comms[0] : nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad local group");
+  }
+  return launch(comms, ncomms, send, recv, count, dtype, op, stream, active_mask, true,
+                NVRAR_PHASE_ALL, order);
 }
 
 int nvrar_reduce_scatter(nvrar_comm_t comm, const void* send, void* recv_shard, size_t count,

@@ -103,7 +103,16 @@ struct LaunchParams {
   uint64_t count;
   int oneshot;  // flat kernel: 1 = one-shot ownership, 0 = two-shot
   int nlocal;
+  int order;    // flat kernel: reduction order, kOrderNvrar / kOrderRing / kOrderTree
+  uint8_t perm[64];  // ring order: global rank at ring position p (ring.hpp:27-30)
 };
+
+// Reduction orders the flat kernel evaluates (the reference's three collectives):
+//   NVRAR — ring fold of the node's ranks per G-chunk, pairwise tree over nodes;
+//   RING  — ring fold of ALL ranks in ring positions per P-chunk (ring.hpp);
+//   TREE  — chain fold in[0] + (in[1] + (... + in[G-1])) per node, pairwise
+//           tree over nodes (tree.hpp:10-12).
+enum : int { kOrderNvrar = 0, kOrderRing = 1, kOrderTree = 2 };
 
 // ---------------------------------------------------------------------------
 // PTX primitives

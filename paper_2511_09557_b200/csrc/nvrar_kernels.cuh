@@ -508,7 +508,10 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const uint64_t n = lp.count;
   const int G = d.gpus, P = d.world, me = d.rank;
   const bool oneshot = lp.oneshot != 0;
-  const uint64_t SG = (n + G - 1) / G;
+  const int order = lp.order;
+  // members of one fold: the node's G ranks, or (ring order) all P ranks
+  const int OG = order == kOrderRing ? P : G;
+  const uint64_t SG = (n + OG - 1) / OG;
   constexpr uint64_t kAlign = UE;
   const uint64_t SP = oneshot ? ((n + kAlign - 1) / kAlign) * kAlign
                               : ((((n + P - 1) / P) + kAlign - 1) / kAlign) * kAlign;
@@ -595,13 +598,17 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
     if (valid == 0) continue;
-    const int c0 = static_cast<int>(e0 / SG32);
-    const bool straddle = e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32;
-    int l0 = c0 + 1;
-    if (l0 >= G) l0 -= G;
+    const bool tree = order == kOrderTree;
+    // the tree chain does not depend on the chunk: one fixed order
+    const int c0 = tree ? 0 : static_cast<int>(e0 / SG32);
+    const bool straddle =
+        !tree && e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32;
+    int l0 = tree ? OG - 1 : c0 + 1;
+    if (l0 >= OG) l0 -= OG;
 
-    // Every source's unit, in fold order relative to c0: r[nn][j] is the copy
-    // of local rank (c0+1+j) % G of node nn.
+    // Every source's unit, in fold order: r[nn][j] is the copy of member
+    // (c0+1+j) % OG of node nn (tree: member OG-1-j; ring: the rank at ring
+    // position (c0+1+j) % P).
     uint32_t r[N][MAXG][RDW];
     uint4* slots[N][MAXG];
     int src[N][MAXG];
@@ -611,9 +618,9 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       int l = l0;
 #pragma unroll
       for (int j = 0; j < MAXG; ++j) {
-        src[nn][j] = nn * G + l;
+        src[nn][j] = order == kOrderRing ? static_cast<int>(lp.perm[l & 63]) : nn * G + l;
         slots[nn][j] = reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(src[nn][j]) * a_stride);
-        if (j < G) {
+        if (j < OG) {
           const int s = src[nn][j];
           if (s == me && u == u_first) {
 #pragma unroll
@@ -623,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
           } else {
             pending |= 1u << (nn * MAXG + j);
           }
-          l = l + 1 == G ? 0 : l + 1;
+          l = tree ? l - 1 : (l + 1 == OG ? 0 : l + 1);
         }
       }
     }
@@ -641,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         raw_to_acc<UE>(E{}, r[nn][0], v);
 #pragma unroll
         for (int j = 1; j < MAXG; ++j) {
-          if (j < G) {
+          if (j < OG) {
             A a[UE];
             raw_to_acc<UE>(E{}, r[nn][j], a);
 #pragma unroll
@@ -654,10 +661,10 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         for (int q = 0; q < UE; ++q) {
           const int cq = q < valid ? static_cast<int>((e0 + q) / SG32) : c0;
           const int rot = cq - c0;
-          A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % G, q);
+          A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % OG, q);
 #pragma unroll
           for (int j = 1; j < MAXG; ++j) {
-            if (j < G) x = acc_add(x, pick<E, UE, RDW, N, MAXG>(r, nn, (j + rot) % G, q));
+            if (j < OG) x = acc_add(x, pick<E, UE, RDW, N, MAXG>(r, nn, (j + rot) % OG, q));
           }
           v[q] = x;
         }

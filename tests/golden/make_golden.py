@@ -106,6 +106,22 @@ def main() -> None:
         x = O.ref_random_inputs(nodes * gpus, w, seed, dt)
         g[f"rd_{dt}_{nodes}x{gpus}_w{w}_s{seed}"] = O.ref_rd_inter(x, nodes, gpus)
 
+    # 8. the reference's baseline collectives: RingAllreduce / TreeAllreduce
+    # result bits (ring.hpp, tree.hpp) per hierarchy, n = 1031, seed 19.
+    bl = {}
+    for nodes, gpus in [(1, 2), (2, 1), (1, 4), (2, 2), (4, 1), (1, 8), (2, 4), (4, 2), (8, 1),
+                        (2, 3), (8, 2)]:
+        x = O.ref_random_inputs(nodes * gpus, 1031, 19, "f32")
+        for which in ("ring", "tree"):
+            out = O.ref_baseline_run_all(which, x, nodes, gpus)
+            assert all(np.array_equal(out[0], out[r]) for r in range(nodes * gpus))
+            bl[f"{which}_{nodes}x{gpus}"] = sha(out[0])
+    g["ring_f32_2x4_n1031_s19"] = O.ref_baseline_run_all(
+        "ring", O.ref_random_inputs(8, 1031, 19, "f32"), 2, 4)[0]
+    g["tree_f32_2x4_n1031_s19"] = O.ref_baseline_run_all(
+        "tree", O.ref_random_inputs(8, 1031, 19, "f32"), 2, 4)[0]
+    meta["baseline_orders_n1031_s19_sha256"] = bl
+
     np.savez_compressed(OUT, **g)
     with open(META, "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)

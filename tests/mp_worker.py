@@ -111,6 +111,26 @@ def main():
             fails += 1
             print(f"rank {rank}: {dtype} rd_inter differs", flush=True)
 
+    # the reference's baseline collectives' orders (ring.hpp / tree.hpp)
+    for order in ("ring", "tree"):
+        if order == "ring" and world > 8:
+            continue
+        for dtype in ("f32", "bf16"):
+            n = 65539
+            x = inputs(dtype, world, n, 950)
+            inp = to_dev(x[rank], dtype)
+            out = torch.empty_like(inp)
+            getattr(comm, f"{order}_allreduce")(inp, out)
+            torch.cuda.synchronize()
+            comm.check()
+            want = O.order_sum(x, args.nodes, args.gpus, order, dtype)
+            got = from_dev(out, dtype)
+            if dtype == "f32":
+                got, want = got.view(np.uint32), want.view(np.uint32)
+            if not np.array_equal(got, want):
+                fails += 1
+                print(f"rank {rank}: {order} {dtype} differs", flush=True)
+
     algos = ["hier", "twoshot", "oneshot"]
     for dtype in ("f32", "bf16", "i32"):
         for algo in algos:

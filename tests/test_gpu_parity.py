@@ -294,3 +294,50 @@ def test_peers_and_sequence_api():
     la, lb = g.plan(1 << 20, torch.bfloat16)
     assert la in ALGOS and lb >= 1
     assert g.plan(1 << 20, torch.bfloat16, active=[0, 1])[0] != "direct"
+
+
+@pytest.mark.parametrize("nodes,gpus", HIERS)
+@pytest.mark.parametrize("order", ["ring", "tree"])
+@pytest.mark.parametrize("algo", ["auto", "oneshot", "twoshot"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+def test_baseline_orders(nodes, gpus, order, algo, dtype):
+    """nvrar_allreduce_local_order: the result bits of the reference's
+    RingAllreduce / TreeAllreduce (ring_order_sum / tree_order_sum, pinned by
+    tests/test_oracle.py against the reference's own runs)."""
+    g = group(nodes, gpus)
+    p = nodes * gpus
+    ring_ok = p <= 8
+    tree_ok = flat_ok(nodes, gpus)
+    g.set_algo(algo)
+    try:
+        for n in (1, 7, 1031, 65539):
+            x = inputs_for(dtype, p, n, 23 + n)
+            ins = [to_dev(x[r], dtype) for r in range(p)]
+            outs = [torch.empty_like(t) for t in ins]
+            if (order == "ring" and not ring_ok) or (order == "tree" and not tree_ok):
+                with pytest.raises(InvalidArgumentError):
+                    g.run_all(ins, outs, order=order)
+                return
+            g.run_all(ins, outs, order=order)
+            want = O.order_sum(x, nodes, gpus, order, dtype)
+            got = np.stack([from_dev(o, dtype) for o in outs])
+            if dtype == "f32":
+                got, want = got.view(np.uint32), want.view(np.uint32)
+            for r in range(p):
+                assert np.array_equal(got[r], want), f"rank {r} differs"
+    finally:
+        g.set_algo("auto")
+
+
+def test_baseline_orders_golden(golden):
+    g_, meta = golden
+    x = O.random_inputs(8, 1031, 19, "f32")
+    grp = group(2, 4)
+    for order in ("ring", "tree"):
+        ins = [to_dev(x[r], "f32") for r in range(8)]
+        outs = [torch.empty_like(t) for t in ins]
+        grp.run_all(ins, outs, order=order)
+        for o in outs:
+            got = from_dev(o, "f32")
+            assert hashlib.sha256(got.tobytes()).hexdigest() == \
+                meta["baseline_orders_n1031_s19_sha256"][f"{order}_2x4"]
