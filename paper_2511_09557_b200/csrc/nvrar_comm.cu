@@ -18,7 +18,7 @@
 
 namespace nvrar {
 using KernelFn = void (*)(LaunchParams);
-KernelFn select_kernel(int dtype, bool flat, int nodes, bool emu, bool lamport);
+KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport);
 KernelFn bump_kernel();
 KernelFn select_direct(int dtype, int nodes);
 KernelFn select_phase(int dtype, int mode, int nodes, bool emu);
@@ -316,7 +316,8 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
       for (int emu = 0; emu < 2; ++emu) {
         int o = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &o, reinterpret_cast<const void*>(select_kernel(dt, flat, c->nodes, emu, true)),
+                &o, reinterpret_cast<const void*>(
+                        select_kernel(dt, flat, c->nodes, std::min(c->gpus, flat_max_gpus(c->nodes)), emu, true)),
                 kThreads, 0) == cudaSuccess &&
             o > 0) {
           occ = flat + dt + emu == 0 ? o : std::min(occ, o);
@@ -720,7 +721,9 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   KernelFn k = phase != NVRAR_PHASE_ALL ? select_phase(dtype, phase, c0->nodes, emu)
                : direct ? select_direct(dtype, c0->nodes)
                         : select_kernel(dtype, algo != NVRAR_ALGO_HIER,
-                                        order == NVRAR_ORDER_RING ? 1 : c0->nodes, emu, lamport);
+                                        order == NVRAR_ORDER_RING ? 1 : c0->nodes,
+                                        order == NVRAR_ORDER_RING ? c0->world : c0->gpus, emu,
+                                        lamport);
   if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
 
   cudaLaunchConfig_t cfg{};

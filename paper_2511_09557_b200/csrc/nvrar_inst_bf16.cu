@@ -1,9 +1,10 @@
-// Instantiates the BF16 kernels (split per dtype so nvcc builds them in parallel).
+// Instantiates the BF16 hierarchical and direct kernels (the flat ones are in
+// nvrar_flat_bf16.cu: one file per group so nvcc builds them in parallel).
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_bf16(bool flat, int nodes, bool emu, bool lamport) {
-  return lamport ? kernel_for<BF16, true>(flat, nodes, emu) : kernel_for<BF16, false>(flat, nodes, emu);
+KernelFn kernel_hier_bf16(int nodes, bool emu, bool lamport) {
+  return lamport ? hier_kernel_for<BF16, true>(nodes, emu) : hier_kernel_for<BF16, false>(nodes, emu);
 }
 KernelFn kernel_direct_bf16(int nodes) { return direct_for<BF16>(nodes); }
 }  // namespace nvrar

@@ -1,9 +1,10 @@
-// Instantiates the F32 kernels (split per dtype so nvcc builds them in parallel).
+// Instantiates the F32 hierarchical and direct kernels (the flat ones are in
+// nvrar_flat_f32.cu: one file per group so nvcc builds them in parallel).
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_f32(bool flat, int nodes, bool emu, bool lamport) {
-  return lamport ? kernel_for<F32, true>(flat, nodes, emu) : kernel_for<F32, false>(flat, nodes, emu);
+KernelFn kernel_hier_f32(int nodes, bool emu, bool lamport) {
+  return lamport ? hier_kernel_for<F32, true>(nodes, emu) : hier_kernel_for<F32, false>(nodes, emu);
 }
 KernelFn kernel_direct_f32(int nodes) { return direct_for<F32>(nodes); }
 }  // namespace nvrar

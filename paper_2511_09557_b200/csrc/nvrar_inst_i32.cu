@@ -1,10 +1,10 @@
-// Instantiates the I32 kernels (split per dtype so nvcc builds them in parallel).
+// Instantiates the I32 hierarchical and direct kernels (flat: nvrar_flat_i32.cu).
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_i32(bool flat, int nodes, bool emu, bool lamport) {
+KernelFn kernel_hier_i32(int nodes, bool emu, bool lamport) {
   (void)lamport;  // int32 has no spare bit pattern: always LL
-  return kernel_for<I32, false>(flat, nodes, emu);
+  return hier_kernel_for<I32, false>(nodes, emu);
 }
 KernelFn kernel_direct_i32(int nodes) { return direct_for<I32>(nodes); }
 }  // namespace nvrar

@@ -554,9 +554,11 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 #pragma unroll
   for (int j = 1; j < kPre; ++j) {
     if (j < P) {
-      const int src = oneshot ? 0 : j;
-      if (pv[src] > 0) {
-        Raw::template put<RDW>(slot_a(d, (me + j) % P, parity, me), u_first, pre[src], c.seq);
+      // compile-time indices only (a runtime index would put pre[] in local memory)
+      if (oneshot) {
+        if (pv[0] > 0) Raw::template put<RDW>(slot_a(d, (me + j) % P, parity, me), u_first, pre[0], c.seq);
+      } else if (pv[j] > 0) {
+        Raw::template put<RDW>(slot_a(d, (me + j) % P, parity, me), u_first, pre[j], c.seq);
       }
     }
   }
@@ -894,26 +896,49 @@ KernelFn hier_for(int nodes) {
   }
 }
 
+// Flat kernels are specialised on MAXG = the next power of two >= gpus per node
+// (register tiles r[N][MAXG] sized to the topology: a 2x1 launch must not
+// carry the 2x8 tile — measured +1.5 us per call at P=2). N * MAXG <= 16.
+template <class E, bool LAMPORT, bool EMU, int N>
+KernelFn flat_for_n(int gpus) {
+  if (gpus <= 1) return flat_kernel<E, LAMPORT, N, 1, EMU>;
+  if (gpus <= 2) return flat_kernel<E, LAMPORT, N, 2, EMU>;
+  if constexpr (N <= 4) {
+    if (gpus <= 4) return flat_kernel<E, LAMPORT, N, 4, EMU>;
+  }
+  if constexpr (N <= 2) {
+    if (gpus <= 8) return flat_kernel<E, LAMPORT, N, 8, EMU>;
+  }
+  return nullptr;
+}
+
 template <class E, bool LAMPORT, bool EMU>
-KernelFn flat_for(int nodes) {
+KernelFn flat_for(int nodes, int gpus) {
   switch (nodes) {
-    case 1: return flat_kernel<E, LAMPORT, 1, 8, EMU>;
-    case 2: return flat_kernel<E, LAMPORT, 2, 8, EMU>;
-    case 4: return flat_kernel<E, LAMPORT, 4, 4, EMU>;
-    case 8: return flat_kernel<E, LAMPORT, 8, 2, EMU>;
+    case 1: return flat_for_n<E, LAMPORT, EMU, 1>(gpus);
+    case 2: return flat_for_n<E, LAMPORT, EMU, 2>(gpus);
+    case 4: return flat_for_n<E, LAMPORT, EMU, 4>(gpus);
+    case 8: return flat_for_n<E, LAMPORT, EMU, 8>(gpus);
     default: return nullptr;
   }
 }
 
 template <class E, bool LAMPORT>
-KernelFn kernel_for(bool flat, int nodes, bool emu) {
-  if (flat) return emu ? flat_for<E, LAMPORT, true>(nodes) : flat_for<E, LAMPORT, false>(nodes);
+KernelFn flat_kernel_for(int nodes, int gpus, bool emu) {
+  return emu ? flat_for<E, LAMPORT, true>(nodes, gpus) : flat_for<E, LAMPORT, false>(nodes, gpus);
+}
+
+template <class E, bool LAMPORT>
+KernelFn hier_kernel_for(int nodes, bool emu) {
   return emu ? hier_for<E, LAMPORT, true>(nodes) : hier_for<E, LAMPORT, false>(nodes);
 }
 
-KernelFn kernel_f32(bool flat, int nodes, bool emu, bool lamport);
-KernelFn kernel_bf16(bool flat, int nodes, bool emu, bool lamport);
-KernelFn kernel_i32(bool flat, int nodes, bool emu, bool lamport);
+KernelFn kernel_hier_f32(int nodes, bool emu, bool lamport);
+KernelFn kernel_hier_bf16(int nodes, bool emu, bool lamport);
+KernelFn kernel_hier_i32(int nodes, bool emu, bool lamport);
+KernelFn kernel_flat_f32(int nodes, int gpus, bool emu, bool lamport);
+KernelFn kernel_flat_bf16(int nodes, int gpus, bool emu, bool lamport);
+KernelFn kernel_flat_i32(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_direct_f32(int nodes);
 KernelFn kernel_direct_bf16(int nodes);
 KernelFn kernel_direct_i32(int nodes);
