@@ -196,7 +196,8 @@ void default_plan(int world, int nodes, uint64_t bytes, bool emu, int* algo, int
     *algo = NVRAR_ALGO_DIRECT;
   } else if (bytes <= one_max) {
     *algo = NVRAR_ALGO_ONESHOT;
-  } else if (bytes <= (2u << 20) && nodes > 1) {
+  } else if (bytes <= (2u << 20) && nodes > 1 && world >= 8) {
+    // P <= 4: two-shot measured faster than the hierarchy above one_max
     *algo = NVRAR_ALGO_HIER;
   } else {
     *algo = NVRAR_ALGO_TWOSHOT;
@@ -317,7 +318,9 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
         int o = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &o, reinterpret_cast<const void*>(
-                        select_kernel(dt, flat, c->nodes, std::min(c->gpus, flat_max_gpus(c->nodes)), emu, true)),
+                        select_kernel(dt, flat, c->nodes,
+                                      flat ? std::min(c->gpus, flat_max_gpus(c->nodes)) : c->gpus,
+                                      emu, true)),
                 kThreads, 0) == cudaSuccess &&
             o > 0) {
           occ = flat + dt + emu == 0 ? o : std::min(occ, o);

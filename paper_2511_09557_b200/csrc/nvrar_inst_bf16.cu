@@ -3,8 +3,9 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_hier_bf16(int nodes, bool emu, bool lamport) {
-  return lamport ? hier_kernel_for<BF16, true>(nodes, emu) : hier_kernel_for<BF16, false>(nodes, emu);
+KernelFn kernel_hier_bf16(int nodes, int gpus, bool emu, bool lamport) {
+  return lamport ? hier_kernel_for<BF16, true>(nodes, gpus, emu)
+                 : hier_kernel_for<BF16, false>(nodes, gpus, emu);
 }
 KernelFn kernel_direct_bf16(int nodes) { return direct_for<BF16>(nodes); }
 }  // namespace nvrar

@@ -3,8 +3,9 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_hier_f32(int nodes, bool emu, bool lamport) {
-  return lamport ? hier_kernel_for<F32, true>(nodes, emu) : hier_kernel_for<F32, false>(nodes, emu);
+KernelFn kernel_hier_f32(int nodes, int gpus, bool emu, bool lamport) {
+  return lamport ? hier_kernel_for<F32, true>(nodes, gpus, emu)
+                 : hier_kernel_for<F32, false>(nodes, gpus, emu);
 }
 KernelFn kernel_direct_f32(int nodes) { return direct_for<F32>(nodes); }
 }  // namespace nvrar

@@ -2,9 +2,9 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_hier_i32(int nodes, bool emu, bool lamport) {
+KernelFn kernel_hier_i32(int nodes, int gpus, bool emu, bool lamport) {
   (void)lamport;  // int32 has no spare bit pattern: always LL
-  return hier_kernel_for<I32, false>(nodes, emu);
+  return hier_kernel_for<I32, false>(nodes, gpus, emu);
 }
 KernelFn kernel_direct_i32(int nodes) { return direct_for<I32>(nodes); }
 }  // namespace nvrar

@@ -195,7 +195,7 @@ __device__ __forceinline__ void group_guard(Ctl& c, const RankDesc& d, uint64_t 
 }
 
 // ---------------------------------------------------------------------------
-template <class E, bool LAMPORT, int N, bool EMU, int MODE = kModeFull>
+template <class E, bool LAMPORT, int N, bool EMU, int MODE = kModeFull, int MG = kHierMaxG>
 __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
   using C = Cfg<E, LAMPORT>;
@@ -222,18 +222,18 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
   const uint64_t u_first = ub + threadIdx.x;
   // grp[j] = (local + j) % G for j < G, without a division per use
-  int grp[kHierMaxG];
+  int grp[MG];
 #pragma unroll
-  for (int j = 0; j < kHierMaxG; ++j) grp[j] = local + j >= G ? local + j - G : local + j;
+  for (int j = 0; j < MG; ++j) grp[j] = local + j >= G ? local + j - G : local + j;
 
   begin_wait(d);
   const SeqWords sw = seq_issue(d);
   // Prefetch this thread's first unit of every chunk while the call number is
   // read (the loads do not depend on it): pre[j] = chunk (local + j) % G.
-  uint32_t pre[kHierMaxG][RDW];
-  int pv[kHierMaxG];
+  uint32_t pre[MG][RDW];
+  int pv[MG];
 #pragma unroll
-  for (int j = 0; j < kHierMaxG; ++j) {
+  for (int j = 0; j < MG; ++j) {
     pv[j] = 0;
     if (kFold && j < G && u_first < ue) {
       const uint64_t cbase = static_cast<uint64_t>(grp[j]) * S;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   // Phase 1a: reduce-scatter pushes (ring_reduce_scatter_phase, ring_schedule.hpp:33-58).
   if (kFold && G > 1) {
 #pragma unroll
-    for (int j = 1; j < kHierMaxG; ++j) {
+    for (int j = 1; j < MG; ++j) {
       if (j < G && pv[j] > 0) {
         Raw::template put<RDW>(slot_a(d, node * G + grp[j], parity, local), u_first,
                                pre[j], c.seq);
@@ -334,21 +334,21 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
         raw_to_acc<UE>(E{}, own, f[k]);
         continue;
       }
-      uint32_t r[1][kHierMaxG - 1][RDW];
-      uint4* slots[1][kHierMaxG - 1];
-      int peers[1][kHierMaxG - 1];
+      uint32_t r[1][MG - 1][RDW];
+      uint4* slots[1][MG - 1];
+      int peers[1][MG - 1];
       uint32_t pending = 0;
 #pragma unroll
-      for (int j = 1; j < kHierMaxG; ++j) {
+      for (int j = 1; j < MG; ++j) {
         slots[0][j - 1] = slot_a(d, me, parity, grp[j]);
         peers[0][j - 1] = node * G + grp[j];
         if (j < G) pending |= 1u << (j - 1);
       }
-      recv_grid<Raw, RDW, 1, kHierMaxG - 1>(c, slots, uu[k], r, pending, peers);
+      recv_grid<Raw, RDW, 1, MG - 1>(c, slots, uu[k], r, pending, peers);
       // c owns in[c] + (in[c-1] + (... + (in[c+2] + in[c+1])))  (ring_schedule.hpp:12-15)
       raw_to_acc<UE>(E{}, r[0][0], f[k]);
 #pragma unroll
-      for (int j = 2; j < kHierMaxG; ++j) {
+      for (int j = 2; j < MG; ++j) {
         if (j < G) {
           A a[UE];
           raw_to_acc<UE>(E{}, r[0][j - 1], a);
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       }
       store_raw<E, UE>(recv, mybase + UE * uu[k], valid[k], o);
 #pragma unroll
-      for (int j = 1; j < kHierMaxG; ++j) {
+      for (int j = 1; j < MG; ++j) {
         if (j < G) {
           Raw::template put<RDW>(slot_b(d, node * G + grp[j], parity, local), uu[k], o, c.seq);
         }
@@ -445,13 +445,13 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   // Phase 3b: all-gather receive.
   if (kGather && G > 1) {
     for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-      uint32_t r[1][kHierMaxG - 1][RDW];
-      uint4* slots[1][kHierMaxG - 1];
-      int peers[1][kHierMaxG - 1];
-      int valid[kHierMaxG - 1];
+      uint32_t r[1][MG - 1][RDW];
+      uint4* slots[1][MG - 1];
+      int peers[1][MG - 1];
+      int valid[MG - 1];
       uint32_t pending = 0;
 #pragma unroll
-      for (int j = 1; j < kHierMaxG; ++j) {
+      for (int j = 1; j < MG; ++j) {
         const int s = grp[j];
         slots[0][j - 1] = slot_b(d, me, parity, s);
         peers[0][j - 1] = node * G + s;
@@ -461,9 +461,9 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
           if (valid[j - 1] > 0) pending |= 1u << (j - 1);
         }
       }
-      recv_grid<Raw, RDW, 1, kHierMaxG - 1>(c, slots, u, r, pending, peers);
+      recv_grid<Raw, RDW, 1, MG - 1>(c, slots, u, r, pending, peers);
 #pragma unroll
-      for (int j = 1; j < kHierMaxG; ++j) {
+      for (int j = 1; j < MG; ++j) {
         if (j < G && valid[j - 1] > 0) {
           store_raw<E, UE>(recv, static_cast<uint64_t>(grp[j]) * S + UE * u, valid[j - 1], r[0][j - 1]);
         }
@@ -885,13 +885,23 @@ KernelFn phase_for(int nodes) {
   }
 }
 
+// The all-reduce kernels are specialised on MG = pow2 >= gpus per node (min 2):
+// the per-member tiles (prefetch, fold sources) are sized to the group.
+template <class E, bool LAMPORT, bool EMU, int N>
+KernelFn hier_for_n(int gpus) {
+  if (gpus <= 2) return hier_kernel<E, LAMPORT, N, EMU, kModeFull, 2>;
+  if (gpus <= 4) return hier_kernel<E, LAMPORT, N, EMU, kModeFull, 4>;
+  if (gpus <= 8) return hier_kernel<E, LAMPORT, N, EMU, kModeFull, 8>;
+  return nullptr;
+}
+
 template <class E, bool LAMPORT, bool EMU>
-KernelFn hier_for(int nodes) {
+KernelFn hier_for(int nodes, int gpus) {
   switch (nodes) {
-    case 1: return hier_kernel<E, LAMPORT, 1, EMU>;
-    case 2: return hier_kernel<E, LAMPORT, 2, EMU>;
-    case 4: return hier_kernel<E, LAMPORT, 4, EMU>;
-    case 8: return hier_kernel<E, LAMPORT, 8, EMU>;
+    case 1: return hier_for_n<E, LAMPORT, EMU, 1>(gpus);
+    case 2: return hier_for_n<E, LAMPORT, EMU, 2>(gpus);
+    case 4: return hier_for_n<E, LAMPORT, EMU, 4>(gpus);
+    case 8: return hier_for_n<E, LAMPORT, EMU, 8>(gpus);
     default: return nullptr;
   }
 }
@@ -929,13 +939,13 @@ KernelFn flat_kernel_for(int nodes, int gpus, bool emu) {
 }
 
 template <class E, bool LAMPORT>
-KernelFn hier_kernel_for(int nodes, bool emu) {
-  return emu ? hier_for<E, LAMPORT, true>(nodes) : hier_for<E, LAMPORT, false>(nodes);
+KernelFn hier_kernel_for(int nodes, int gpus, bool emu) {
+  return emu ? hier_for<E, LAMPORT, true>(nodes, gpus) : hier_for<E, LAMPORT, false>(nodes, gpus);
 }
 
-KernelFn kernel_hier_f32(int nodes, bool emu, bool lamport);
-KernelFn kernel_hier_bf16(int nodes, bool emu, bool lamport);
-KernelFn kernel_hier_i32(int nodes, bool emu, bool lamport);
+KernelFn kernel_hier_f32(int nodes, int gpus, bool emu, bool lamport);
+KernelFn kernel_hier_bf16(int nodes, int gpus, bool emu, bool lamport);
+KernelFn kernel_hier_i32(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_flat_f32(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_flat_bf16(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_flat_i32(int nodes, int gpus, bool emu, bool lamport);

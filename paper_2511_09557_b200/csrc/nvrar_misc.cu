@@ -51,9 +51,9 @@ __global__ void pingpong_kernel(const __grid_constant__ LaunchParams lp, int pee
 
 KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport) {
   switch (dtype) {
-    case 0: return flat ? kernel_flat_i32(nodes, gpus, emu, false) : kernel_hier_i32(nodes, emu, false);
-    case 1: return flat ? kernel_flat_f32(nodes, gpus, emu, lamport) : kernel_hier_f32(nodes, emu, lamport);
-    case 2: return flat ? kernel_flat_bf16(nodes, gpus, emu, lamport) : kernel_hier_bf16(nodes, emu, lamport);
+    case 0: return flat ? kernel_flat_i32(nodes, gpus, emu, false) : kernel_hier_i32(nodes, gpus, emu, false);
+    case 1: return flat ? kernel_flat_f32(nodes, gpus, emu, lamport) : kernel_hier_f32(nodes, gpus, emu, lamport);
+    case 2: return flat ? kernel_flat_bf16(nodes, gpus, emu, lamport) : kernel_hier_bf16(nodes, gpus, emu, lamport);
     default: return nullptr;
   }
 }
