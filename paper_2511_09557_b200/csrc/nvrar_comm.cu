@@ -20,7 +20,7 @@ namespace nvrar {
 using KernelFn = void (*)(LaunchParams);
 KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport);
 KernelFn bump_kernel();
-KernelFn select_direct(int dtype, int nodes);
+KernelFn select_direct(int dtype, int nodes, int gpus);
 KernelFn select_phase(int dtype, int mode, int nodes, bool emu);
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);
 PingFn pingpong_fn();
@@ -333,7 +333,7 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   for (int dt = 0; dt < 3; ++dt) {
     int o = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &o, reinterpret_cast<const void*>(select_direct(dt, c->nodes)), kDirectThreads, 0) !=
+            &o, reinterpret_cast<const void*>(select_direct(dt, c->nodes, c->gpus)), kDirectThreads, 0) !=
         cudaSuccess) {
       o = 1;
     }
@@ -722,7 +722,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   lp.d0 = c0->h_desc;
   const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
   KernelFn k = phase != NVRAR_PHASE_ALL ? select_phase(dtype, phase, c0->nodes, emu)
-               : direct ? select_direct(dtype, c0->nodes)
+               : direct ? select_direct(dtype, c0->nodes, c0->gpus)
                         : select_kernel(dtype, algo != NVRAR_ALGO_HIER,
                                         order == NVRAR_ORDER_RING ? 1 : c0->nodes,
                                         order == NVRAR_ORDER_RING ? c0->world : c0->gpus, emu,

@@ -7,5 +7,5 @@ KernelFn kernel_hier_bf16(int nodes, int gpus, bool emu, bool lamport) {
   return lamport ? hier_kernel_for<BF16, true>(nodes, gpus, emu)
                  : hier_kernel_for<BF16, false>(nodes, gpus, emu);
 }
-KernelFn kernel_direct_bf16(int nodes) { return direct_for<BF16>(nodes); }
+KernelFn kernel_direct_bf16(int nodes, int gpus) { return direct_for<BF16>(nodes, gpus); }
 }  // namespace nvrar

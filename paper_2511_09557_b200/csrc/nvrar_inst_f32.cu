@@ -7,5 +7,5 @@ KernelFn kernel_hier_f32(int nodes, int gpus, bool emu, bool lamport) {
   return lamport ? hier_kernel_for<F32, true>(nodes, gpus, emu)
                  : hier_kernel_for<F32, false>(nodes, gpus, emu);
 }
-KernelFn kernel_direct_f32(int nodes) { return direct_for<F32>(nodes); }
+KernelFn kernel_direct_f32(int nodes, int gpus) { return direct_for<F32>(nodes, gpus); }
 }  // namespace nvrar

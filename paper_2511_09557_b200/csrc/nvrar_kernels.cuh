@@ -863,13 +863,25 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
 
 using KernelFn = void (*)(LaunchParams);
 
+// MAXG = pow2 >= gpus per node (the per-thread source tile r[N][MAXG]), N * MAXG <= 32.
+template <class E, int N>
+KernelFn direct_for_n(int gpus) {
+  if (gpus <= 1) return direct_kernel<E, N, 1>;
+  if (gpus <= 2) return direct_kernel<E, N, 2>;
+  if (gpus <= 4) return direct_kernel<E, N, 4>;
+  if constexpr (N <= 4) {
+    if (gpus <= 8) return direct_kernel<E, N, 8>;
+  }
+  return nullptr;
+}
+
 template <class E>
-KernelFn direct_for(int nodes) {
+KernelFn direct_for(int nodes, int gpus) {
   switch (nodes) {
-    case 1: return direct_kernel<E, 1, 8>;
-    case 2: return direct_kernel<E, 2, 8>;
-    case 4: return direct_kernel<E, 4, 8>;
-    case 8: return direct_kernel<E, 8, 4>;
+    case 1: return direct_for_n<E, 1>(gpus);
+    case 2: return direct_for_n<E, 2>(gpus);
+    case 4: return direct_for_n<E, 4>(gpus);
+    case 8: return direct_for_n<E, 8>(gpus);
     default: return nullptr;
   }
 }
@@ -949,9 +961,9 @@ KernelFn kernel_hier_i32(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_flat_f32(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_flat_bf16(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_flat_i32(int nodes, int gpus, bool emu, bool lamport);
-KernelFn kernel_direct_f32(int nodes);
-KernelFn kernel_direct_bf16(int nodes);
-KernelFn kernel_direct_i32(int nodes);
+KernelFn kernel_direct_f32(int nodes, int gpus);
+KernelFn kernel_direct_bf16(int nodes, int gpus);
+KernelFn kernel_direct_i32(int nodes, int gpus);
 KernelFn kernel_phase_f32(int mode, int nodes, bool emu);
 KernelFn kernel_phase_bf16(int mode, int nodes, bool emu);
 KernelFn kernel_phase_i32(int mode, int nodes, bool emu);

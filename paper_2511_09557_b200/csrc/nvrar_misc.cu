@@ -58,11 +58,11 @@ KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool
   }
 }
 
-KernelFn select_direct(int dtype, int nodes) {
+KernelFn select_direct(int dtype, int nodes, int gpus) {
   switch (dtype) {
-    case 0: return kernel_direct_i32(nodes);
-    case 1: return kernel_direct_f32(nodes);
-    case 2: return kernel_direct_bf16(nodes);
+    case 0: return kernel_direct_i32(nodes, gpus);
+    case 1: return kernel_direct_f32(nodes, gpus);
+    case 2: return kernel_direct_bf16(nodes, gpus);
     default: return nullptr;
   }
 }
