@@ -21,6 +21,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ccsim/collectives/fused.hpp"  // Element, NvrarConfig
@@ -77,6 +78,50 @@ class NvrarB200Allreduce {
     throw_on(nvrar_check(comm_), comm_);  // synchronises; device faults -> exceptions
   }
 
+  /// Inter-node phase only (NvrarAllreduce<T>::rd_inter, nvrar.hpp:132-155):
+  /// `packed` = this rank's shard as fused words {data, seq} packed with
+  /// sequence()+1; `out` receives the reduced shard packed with that call.
+  void rd_inter(std::span<const std::uint64_t> packed, std::span<std::uint64_t> out,
+                const NvrarConfig& cfg = {}, void* stream = nullptr) {
+    cfg.validate();
+    if (packed.size() != out.size()) throw InvalidArgumentError("rd_inter: bad shard length");
+    throw_on(nvrar_set_config(comm_, cfg.blocks, cfg.chunk_bytes), comm_);
+    throw_on(nvrar_rd_inter(comm_, packed.data(), out.data(), packed.size(), dtype(), stream),
+             comm_);
+    throw_on(nvrar_check(comm_), comm_);
+  }
+
+  /// IntraReduceScatter<T>::run (nvrar.hpp:280-299) over this rank's node:
+  /// `shard` gets ceil(n / gpus_per_node) elements of the node-local sum.
+  void reduce_scatter(std::span<const T> in, std::span<T> shard, void* stream = nullptr) {
+    throw_on(nvrar_reduce_scatter(comm_, in.data(), shard.data(), in.size(), dtype(), NVRAR_SUM,
+                                  stream),
+             comm_);
+    throw_on(nvrar_check(comm_), comm_);
+  }
+
+  /// IntraAllGather<T>::run (nvrar.hpp:348-364) over this rank's node.
+  void all_gather(std::span<const T> shard, std::span<T> out, void* stream = nullptr) {
+    throw_on(nvrar_all_gather(comm_, shard.data(), out.data(), shard.size(), dtype(), stream),
+             comm_);
+    throw_on(nvrar_check(comm_), comm_);
+  }
+
+  /// The result bits of RingAllreduce<T>::run / TreeAllreduce<T>::run
+  /// (ring.hpp, tree.hpp) on the same communicator.
+  void run_ring(std::span<const T> in, std::span<T> out, void* stream = nullptr) {
+    throw_on(nvrar_ring_allreduce(comm_, in.data(), out.data(), in.size(), dtype(), NVRAR_SUM,
+                                  stream),
+             comm_);
+    throw_on(nvrar_check(comm_), comm_);
+  }
+  void run_tree(std::span<const T> in, std::span<T> out, void* stream = nullptr) {
+    throw_on(nvrar_tree_allreduce(comm_, in.data(), out.data(), in.size(), dtype(), NVRAR_SUM,
+                                  stream),
+             comm_);
+    throw_on(nvrar_check(comm_), comm_);
+  }
+
   /// Step-l exchange peers (nvrar.hpp:158).
   std::vector<RankId> peers(const ClusterTopology& topo) const {
     int p[8];
@@ -116,6 +161,37 @@ class NvrarB200Allreduce {
 
   nvrar_comm_t comm_ = nullptr;
   std::size_t max_elems_;
+};
+
+/// Drop-ins for the reference's baseline collectives (RingAllreduce<T>,
+/// TreeAllreduce<T>): the same constructor as NvrarB200Allreduce, `run(in, out)`
+/// gives the reference's result bits for that algorithm's reduction order.
+template <Element T>
+class B200RingAllreduce {
+ public:
+  template <class... A>
+  explicit B200RingAllreduce(A&&... a) : impl_(std::forward<A>(a)...) {}
+  void run(std::span<const T> in, std::span<T> out, void* stream = nullptr) {
+    impl_.run_ring(in, out, stream);
+  }
+  std::uint32_t sequence() const { return impl_.sequence(); }
+
+ private:
+  NvrarB200Allreduce<T> impl_;
+};
+
+template <Element T>
+class B200TreeAllreduce {
+ public:
+  template <class... A>
+  explicit B200TreeAllreduce(A&&... a) : impl_(std::forward<A>(a)...) {}
+  void run(std::span<const T> in, std::span<T> out, void* stream = nullptr) {
+    impl_.run_tree(in, out, stream);
+  }
+  std::uint32_t sequence() const { return impl_.sequence(); }
+
+ private:
+  NvrarB200Allreduce<T> impl_;
 };
 
 }  // namespace ccsim

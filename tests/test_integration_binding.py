@@ -16,13 +16,40 @@ REF_INC = "/root/reference/proj/include"
 PROGRAM = r'''
 #include <cstdio>
 #include "ccsim_nvrar_b200.hpp"
+// every drop-in entry point must compile against the reference headers
+template <class T>
+void uses(ccsim::NvrarB200Allreduce<T>& c) {
+  std::span<const T> in;
+  std::span<T> out;
+  std::span<const std::uint64_t> pk;
+  std::span<std::uint64_t> po;
+  c.run(in, out, ccsim::NvrarConfig{}, nullptr);
+  c.rd_inter(pk, po, ccsim::NvrarConfig{}, nullptr);
+  c.reduce_scatter(in, out, nullptr);
+  c.all_gather(in, out, nullptr);
+  c.run_ring(in, out, nullptr);
+  c.run_tree(in, out, nullptr);
+}
+template void uses<float>(ccsim::NvrarB200Allreduce<float>&);
+template void uses<std::int32_t>(ccsim::NvrarB200Allreduce<std::int32_t>&);
+
 int main() {
   try {
     ccsim::NvrarB200Allreduce<float> bad(ccsim::ClusterTopology{3, 1}, 0, 0, 1024, nullptr,
                                          nullptr);
   } catch (const ccsim::InvalidTopologyError& e) {
     std::printf("InvalidTopologyError: %s\n", e.what());
-    return 0;
+    try {
+      ccsim::B200RingAllreduce<float> r(ccsim::ClusterTopology{3, 1}, 0, 0, 1024, nullptr,
+                                        nullptr);
+    } catch (const ccsim::InvalidTopologyError&) {
+      try {
+        ccsim::B200TreeAllreduce<std::int32_t> t(ccsim::ClusterTopology{6, 1}, 0, 0, 1024,
+                                                 nullptr, nullptr);
+      } catch (const ccsim::InvalidTopologyError&) {
+        return 0;
+      }
+    }
   }
   return 1;
 }
