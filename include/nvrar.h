@@ -171,6 +171,20 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
                           void* const* recv, size_t count, nvrar_dtype_t dtype, nvrar_op_t op,
                           void* stream, uint64_t active_mask);
 
+/* Fused epilogue for the TP-decode caller (x = x + all_reduce(a), SURVEY §8f
+ * row 2): recv[i] = residual[i] + sum_r send_r[i], where the sum is the
+ * all-reduce's own result (same bits as nvrar_allreduce) and the add is the
+ * element type's (bf16: fp32 add of the two bf16 values, one RNE) — bit-
+ * identical to the unfused all-reduce followed by an elementwise add, without
+ * the extra kernel and memory pass. recv may alias residual (in place). */
+int nvrar_allreduce_residual(nvrar_comm_t comm, const void* send, void* recv,
+                             const void* residual, size_t count, nvrar_dtype_t dtype,
+                             nvrar_op_t op, void* stream);
+int nvrar_allreduce_local_residual(nvrar_comm_t* comms, int ncomms, const void* const* send,
+                                   void* const* recv, const void* const* residual, size_t count,
+                                   nvrar_dtype_t dtype, nvrar_op_t op, void* stream,
+                                   uint64_t active_mask);
+
 /* ---- the reference's baseline collectives --------------------------------
  * The same sum with the reduction ORDER of the reference's other two
  * all-reduces, for model validation against them (they run on the flat

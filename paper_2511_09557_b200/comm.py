@@ -309,6 +309,19 @@ class Communicator:
         if rc:
             _raise(rc, self.last_error(), self.rank)
 
+    def allreduce_residual(self, send: torch.Tensor, residual: torch.Tensor,
+                           out: Optional[torch.Tensor] = None,
+                           stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """out = residual + all_reduce(send) in one kernel (out defaults to residual,
+        i.e. in place) — the TP-decode `x = x + all_reduce(a)`."""
+        _check_pair(send, residual)
+        out = residual if out is None else out
+        _check_pair(send, out)
+        self._check(self._lib.nvrar_allreduce_residual(
+            self._h, send.data_ptr(), out.data_ptr(), residual.data_ptr(), send.numel(),
+            dtype_code(send.dtype), L.SUM, _stream_ptr(stream)))
+        return out
+
     # ---- the reference's baseline collectives (ring.hpp / tree.hpp orders) ----
     def ring_allreduce(self, send: torch.Tensor, recv: torch.Tensor,
                        stream: Optional[torch.cuda.Stream] = None) -> None:
@@ -502,7 +515,8 @@ class LocalGroup:
 
     def launch(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
                active: Optional[Sequence[int]] = None,
-               stream: Optional[torch.cuda.Stream] = None, order: str = "nvrar") -> None:
+               stream: Optional[torch.cuda.Stream] = None, order: str = "nvrar",
+               residuals: Optional[Sequence[torch.Tensor]] = None) -> None:
         p = self.topo.world_size()
         if len(inputs) != p or len(outputs) != p:
             raise InvalidArgumentError("one input and one output per rank")
@@ -513,7 +527,13 @@ class LocalGroup:
         send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
         recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])
         mask = (1 << 64) - 1 if active is None else sum(1 << r for r in active)
-        if order == "nvrar":
+        if residuals is not None:
+            for x in residuals:
+                _check_pair(inputs[0], x)
+            res = (ctypes.c_void_p * p)(*[t.data_ptr() for t in residuals])
+            rc = self._lib.nvrar_allreduce_local_residual(self._arr, p, send, recv, res, n, dt,
+                                                          L.SUM, _stream_ptr(stream), mask)
+        elif order == "nvrar":
             rc = self._lib.nvrar_allreduce_local(self._arr, p, send, recv, n, dt, L.SUM,
                                                  _stream_ptr(stream), mask)
         else:

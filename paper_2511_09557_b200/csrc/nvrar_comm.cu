@@ -626,7 +626,8 @@ static size_t phase_bytes(const nvrar_comm* c, int phase, size_t count, int dtyp
 
 static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void* const* recv,
                   size_t count, int dtype, int op, void* stream, uint64_t mask, bool local_group,
-                  int phase = NVRAR_PHASE_ALL, int order = NVRAR_ORDER_NVRAR) {
+                  int phase = NVRAR_PHASE_ALL, int order = NVRAR_ORDER_NVRAR,
+                  const void* const* resid = nullptr) {
   nvrar_comm* c0 = comms[0];
   if (op != NVRAR_SUM) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "only SUM is supported");
   if (order < NVRAR_ORDER_NVRAR || order > NVRAR_ORDER_TREE) {
@@ -677,6 +678,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
     lp.desc[nl] = c->d_desc;
     lp.send[nl] = send[i];
     lp.recv[nl] = recv[i];
+    lp.resid[nl] = resid ? resid[i] : nullptr;
     ++nl;
   }
   if (nl == 0) return NVRAR_SUCCESS;
@@ -759,6 +761,29 @@ int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t coun
   const void* s[1] = {send};
   void* r[1] = {recv};
   return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false);
+}
+
+int nvrar_allreduce_residual(nvrar_comm_t comm, const void* send, void* recv,
+                             const void* residual, size_t count, nvrar_dtype_t dtype,
+                             nvrar_op_t op, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  if (count > 0 && !residual) return fail(comm, NVRAR_ERR_INVALID_ARGUMENT, "null residual");
+  const void* s[1] = {send};
+  void* r[1] = {recv};
+  const void* x[1] = {residual};
+  return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false, NVRAR_PHASE_ALL,
+                NVRAR_ORDER_NVRAR, x);
+}
+
+int nvrar_allreduce_local_residual(nvrar_comm_t* comms, int ncomms, const void* const* send,
+                                   void* const* recv, const void* const* residual, size_t count,
+                                   nvrar_dtype_t dtype, nvrar_op_t op, void* stream,
+                                   uint64_t active_mask) {
+  if (!comms || ncomms < 1 || ncomms > NVRAR_MAX_LOCAL || !send || !recv || !residual) {
+    return fail(comms ? comms[0] : nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad local group");
+  }
+  return launch(comms, ncomms, send, recv, count, dtype, op, stream, active_mask, true,
+                NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, residual);
 }
 
 int nvrar_ring_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,

@@ -105,6 +105,10 @@ struct LaunchParams {
   int nlocal;
   int order;    // flat kernel: reduction order, kOrderNvrar / kOrderRing / kOrderTree
   uint8_t perm[64];  // ring order: global rank at ring position p (ring.hpp:27-30)
+  // fused residual epilogue (nvrar_allreduce_residual): recv = resid + sum,
+  // with the element type's own add (bf16: fp32 add of the rounded sum, one
+  // RNE) — bit-identical to the all-reduce followed by `resid + out`
+  const void* resid[kMaxLocal];
 };
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):
@@ -648,6 +652,27 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 
 __device__ __forceinline__ void stamp(const RankDesc& d, int k) {
   if (d.profile && threadIdx.x == 0) d.state->ts[blockIdx.x][k] = globaltimer();
+}
+
+// Final store of an output unit: plain, or fused with the residual add.
+template <class E, int UE>
+__device__ __forceinline__ void emit(void* recv, const void* resid, uint64_t e, int valid,
+                                     const uint32_t (&o)[UE * E::kBytes / 4]) {
+  if (resid == nullptr) {
+    store_raw<E, UE>(recv, e, valid, o);
+    return;
+  }
+  using A = typename E::acc;
+  uint32_t x[UE * E::kBytes / 4];
+  load_raw<E, UE>(resid, e, valid, x);
+  A xa[UE], oa[UE];
+  raw_to_acc<UE>(E{}, x, xa);
+  raw_to_acc<UE>(E{}, o, oa);
+#pragma unroll
+  for (int q = 0; q < UE; ++q) xa[q] = acc_add(xa[q], oa[q]);
+  uint32_t r[UE * E::kBytes / 4];
+  acc_to_raw<UE>(E{}, xa, r);
+  store_raw<E, UE>(recv, e, valid, r);
 }
 
 }  // namespace nvrar

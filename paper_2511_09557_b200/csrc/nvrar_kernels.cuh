@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
   void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
+  const void* resid = EMU ? lp.resid[blockIdx.y] : lp.resid[0];
   const uint64_t u_first = ub + threadIdx.x;
   // grp[j] = (local + j) % G for j < G, without a division per use
   int grp[MG];
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       } else {
         acc_to_raw<UE>(E{}, f[k], o);
       }
-      store_raw<E, UE>(recv, mybase + UE * uu[k], valid[k], o);
+      emit<E, UE>(recv, resid, mybase + UE * uu[k], valid[k], o);
 #pragma unroll
       for (int j = 1; j < MG; ++j) {
         if (j < G) {
@@ -465,7 +466,8 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
       for (int j = 1; j < MG; ++j) {
         if (j < G && valid[j - 1] > 0) {
-          store_raw<E, UE>(recv, static_cast<uint64_t>(grp[j]) * S + UE * u, valid[j - 1], r[0][j - 1]);
+          emit<E, UE>(recv, resid, static_cast<uint64_t>(grp[j]) * S + UE * u, valid[j - 1],
+                      r[0][j - 1]);
         }
       }
     }
@@ -520,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
   void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
+  const void* resid = EMU ? lp.resid[blockIdx.y] : lp.resid[0];
   const uint64_t u_first = ub + threadIdx.x;
 
   begin_wait(d);
@@ -690,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
     uint32_t o[RDW];
     acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
-    store_raw<E, UE>(recv, e0, valid, o);
+    emit<E, UE>(recv, resid, e0, valid, o);
     if (!oneshot) {
       int q = me;
       for (int j = 1; j < P; ++j) {
@@ -732,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 #pragma unroll
         for (int t = 0; t < kGrp; ++t) {
           if (valid[t] > 0) {
-            store_raw<E, UE>(recv, static_cast<uint32_t>(qs[0][t] * SP) + UE * static_cast<uint32_t>(u),
+            emit<E, UE>(recv, resid, static_cast<uint32_t>(qs[0][t] * SP) + UE * static_cast<uint32_t>(u),
                              valid[t], r[0][t]);
           }
         }
@@ -847,7 +850,7 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
     acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
     u += blockDim.x;
     if (u < ue) load_unit(u);
-    for (int r2 = 0; r2 < P; ++r2) store_raw<E, UE>(lp.recv[r2], e0, valid, o);
+    for (int r2 = 0; r2 < P; ++r2) emit<E, UE>(lp.recv[r2], lp.resid[r2], e0, valid, o);
   }
   // Nothing here waits on a peer, so the call number is never needed: advance
   // this CTA's replicated counter slots by one without reading them (a sticky

@@ -64,3 +64,17 @@ def all_reduce_(x: torch.Tensor, comm_id: int) -> None:
 @all_reduce_.register_fake
 def _all_reduce__fake(x: torch.Tensor, comm_id: int) -> None:
     return None
+
+
+@torch.library.custom_op("nvrar::all_reduce_residual_", mutates_args=("residual",))
+def all_reduce_residual_(x: torch.Tensor, residual: torch.Tensor, comm_id: int) -> None:
+    """residual += all_reduce(x), fused into the all-reduce's final store (one
+    kernel; bit-identical to all_reduce followed by the add)."""
+    if not (x.is_contiguous() and residual.is_contiguous()):
+        raise ValueError("nvrar::all_reduce_residual_: tensors must be contiguous")
+    _comm(comm_id).allreduce_residual(x, residual)
+
+
+@all_reduce_residual_.register_fake
+def _all_reduce_residual__fake(x: torch.Tensor, residual: torch.Tensor, comm_id: int) -> None:
+    return None

@@ -13,7 +13,8 @@ ranks.
 Per layer and rank (Llama-3.1 shapes, bf16, random weights):
     h  = rmsnorm(x) @ W_qkv[:, shard]         column-parallel (q, k, v heads / TP)
     a  = h[:, :hidden/TP] @ W_o[shard, :]     row-parallel -> all-reduce #1
-    x  = x + a
+    x  = x + a                                (arm "nvrar_fused": one kernel,
+                                               nvrar_allreduce_residual)
     g  = rmsnorm(x) @ W_gate_up[:, shard]     column-parallel (2 * ffn / TP)
     d  = (silu(g1) * g2) @ W_down[shard, :]   row-parallel -> all-reduce #2
     x  = x + d
@@ -98,24 +99,28 @@ class TpDecodeSkeleton:
     def weight_bytes_per_layer(self) -> int:
         return sum(t.numel() * t.element_size() for t in self.sets[0].values())
 
-    def step(self, all_reduce) -> None:
-        """One decode step over all layers; all_reduce(t) sums t in place over ranks
-        (None = skip the collective, for the compute-only reference)."""
+    def step(self, all_reduce, fused_residual=None) -> None:
+        """One decode step over all layers. all_reduce(t) sums t in place over ranks
+        (None = skip the collective, for the compute-only reference);
+        fused_residual(t, x), when given, does x += all_reduce(t) in one kernel."""
         x = self.x
         x.copy_(self.x0)
         hs = self.hidden // self.tp
+
+        def add_reduced(t):
+            if fused_residual is not None:
+                fused_residual(t, x)
+                return
+            if all_reduce is not None:
+                all_reduce(t)
+            x.add_(t)
+
         for layer in range(self.layers):
             W = self.sets[layer % len(self.sets)]
             qkv = F.rms_norm(x, (self.hidden,)) @ W["qkv"]
-            a = qkv[:, :hs] @ W["o"]
-            if all_reduce is not None:
-                all_reduce(a)
-            x = x + a
+            add_reduced(qkv[:, :hs] @ W["o"])
             gu = F.rms_norm(x, (self.hidden,)) @ W["gu"]
-            d = (F.silu(gu[:, :self.ffn_shard]) * gu[:, self.ffn_shard:]) @ W["down"]
-            if all_reduce is not None:
-                all_reduce(d)
-            x = x + d
+            add_reduced((F.silu(gu[:, :self.ffn_shard]) * gu[:, self.ffn_shard:]) @ W["down"])
         self.out = x
 
 
@@ -189,14 +194,18 @@ def main() -> None:
     def nccl_ar(t):
         dist.all_reduce(t)
 
+    def nvrar_fused(t, x):
+        torch.ops.nvrar.all_reduce_residual_(t, x, cid)
+
     for batch in batches:
         wl = DecodeWorkload(batch, cfg["hidden"], 2, args.layers or cfg["layers"])
         m = TpDecodeSkeleton(args.model, batch, tp, torch.device("cuda", local),
                              layers=args.layers or None)
         res = {}
         outs = {}
-        for name, ar in (("nvrar", nvrar_ar), ("nccl", nccl_ar), ("compute_only", None)):
-            gr = _graph(lambda: m.step(ar))
+        for name, ar, fu in (("nvrar", nvrar_ar, None), ("nvrar_fused", None, nvrar_fused),
+                             ("nccl", nccl_ar, None), ("compute_only", None, None)):
+            gr = _graph(lambda: m.step(ar, fu))
             ts = _time(gr, args.iters, args.warmup)
             res[name] = statistics.median(ts)
             outs[name] = m.out.float().clone()
@@ -204,6 +213,8 @@ def main() -> None:
         comm.check()
         # both collectives must give the same model output (bf16 sums, different orders)
         diff = float((outs["nvrar"] - outs["nccl"]).abs().max())
+        # the fused epilogue must reproduce the unfused NVRAR step bit for bit
+        fused_equal = bool(torch.equal(outs["nvrar"], outs["nvrar_fused"]))
         scale = float(outs["nccl"].abs().max())
         if rank == 0:
             comm_nv = res["nvrar"] - res["compute_only"]
@@ -216,6 +227,8 @@ def main() -> None:
                 "per_allreduce_us": {"nvrar": round(comm_nv * 1e3 / wl.allreduces_per_step(), 3),
                                      "nccl": round(comm_nc * 1e3 / wl.allreduces_per_step(), 3)},
                 "step_speedup_vs_nccl": round(res["nccl"] / res["nvrar"], 4),
+                "fused_step_speedup_vs_nccl": round(res["nccl"] / res["nvrar_fused"], 4),
+                "fused_bit_identical": fused_equal,
                 "weight_mb_per_layer": round(m.weight_bytes_per_layer() / 2**20, 1),
                 "max_abs_diff_vs_nccl": diff, "out_scale": scale,
                 "timing": "CUDA graph of one full step, CUDA events, max over ranks, median",

@@ -111,6 +111,26 @@ def main():
             fails += 1
             print(f"rank {rank}: {dtype} rd_inter differs", flush=True)
 
+    # fused residual epilogue: out = residual + all_reduce(x), in place
+    for dtype in ("f32", "bf16"):
+        n = 65539
+        x = inputs(dtype, world, n, 960)
+        res = inputs(dtype, world, n, 961)
+        r_dev = to_dev(res[rank], dtype)
+        comm.allreduce_residual(to_dev(x[rank], dtype), r_dev)
+        torch.cuda.synchronize()
+        comm.check()
+        want = O.nvrar_order_sum(x, args.nodes, args.gpus, dtype)
+        if dtype == "f32":
+            exp = (want + res[rank]).view(np.uint32)
+            got = from_dev(r_dev, dtype).view(np.uint32)
+        else:
+            exp = O.bf16_bits_from_f32(O.f32_from_bf16_bits(want) + O.f32_from_bf16_bits(res[rank]))
+            got = from_dev(r_dev, dtype)
+        if not np.array_equal(got, exp):
+            fails += 1
+            print(f"rank {rank}: fused residual {dtype} differs", flush=True)
+
     # the reference's baseline collectives' orders (ring.hpp / tree.hpp)
     for order in ("ring", "tree"):
         if order == "ring" and world > 8:

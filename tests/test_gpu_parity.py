@@ -341,3 +341,45 @@ def test_baseline_orders_golden(golden):
             got = from_dev(o, "f32")
             assert hashlib.sha256(got.tobytes()).hexdigest() == \
                 meta["baseline_orders_n1031_s19_sha256"][f"{order}_2x4"]
+
+
+def _add_like(want, resid, dtype):
+    """The element type's own add (what `residual + all_reduce(x)` gives)."""
+    if dtype == "f32":
+        return (want.view(np.float32) + resid.view(np.float32)).view(np.uint32)
+    if dtype == "bf16":
+        return O.bf16_bits_from_f32(O.f32_from_bf16_bits(want) + O.f32_from_bf16_bits(resid))
+    with np.errstate(over="ignore"):
+        return (want.astype(np.int64) + resid.astype(np.int64)).astype(np.int32)
+
+
+@pytest.mark.parametrize("nodes,gpus", [(1, 2), (2, 2), (2, 4), (4, 2), (8, 1), (2, 3)])
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_allreduce_residual_fused(nodes, gpus, algo, dtype, inplace):
+    """nvrar_allreduce_local_residual: out = residual + all_reduce(x), bit-identical
+    to the all-reduce followed by the element type's add."""
+    if algo in ("twoshot", "oneshot") and not flat_ok(nodes, gpus):
+        pytest.skip("flat schedules")
+    g = group(nodes, gpus)
+    p = nodes * gpus
+    g.set_algo(algo)
+    try:
+        for n in (7, 1031, 65539):
+            x = inputs_for(dtype, p, n, 61 + n)
+            res = inputs_for(dtype, p, n, 62 + n)
+            ins = [to_dev(x[r], dtype) for r in range(p)]
+            rs = [to_dev(res[r], dtype) for r in range(p)]
+            outs = rs if inplace else [torch.empty_like(t) for t in ins]
+            g.launch(ins, outs, residuals=rs)
+            g.check()
+            want = O.nvrar_order_sum(x, nodes, gpus, dtype)
+            if dtype == "f32":
+                want = want.view(np.uint32)
+            for r in range(p):
+                got = from_dev(outs[r], dtype)
+                exp = _add_like(want, res[r].view(np.uint32) if dtype == "f32" else res[r], dtype)
+                assert np.array_equal(got.view(exp.dtype), exp), f"rank {r}"
+    finally:
+        g.set_algo("auto")
