@@ -282,6 +282,9 @@ def run_multi(args, rank, world, local):
     dev = torch.device("cuda", local)
 
     alpha = H.alpha_signal_us(comm, rank, world)
+    # NVLS multicast one-shot as a selector candidate (collective setup; any
+    # rank failing disables it everywhere)
+    mc_ok = False if args.no_multicast else comm.enable_multicast()
     tuned = None
     if not args.no_autotune:
         tuned = S.autotune(comm, sizes=SWEEP, dtype=torch.bfloat16, calls=30, reps=5)
@@ -358,7 +361,7 @@ def run_multi(args, rank, world, local):
                    "roofline_us": round(rt, 3), "roofline_frac": round(rt / v, 3)}
             if tuned is not None:
                 cands = tuned["measured"][size]
-                for a_name in ("hier", "twoshot", "oneshot"):
+                for a_name in ("hier", "twoshot", "oneshot", "mcast"):
                     vals = [t for k, t in cands.items() if k.startswith(a_name + "/")]
                     if vals:
                         row[f"{a_name}_best_us"] = min(vals)
@@ -378,6 +381,7 @@ def run_multi(args, rank, world, local):
                        "nodes": nodes, "gpus_per_node": gpus, "message_bytes": msg,
                        "algo": plan[0], "blocks_per_rank": plan[1], "calls_per_step": calls,
                        "selector": "autotuned on this box" if tuned else "built-in policy",
+                       "multicast": mc_ok,
                        "selector_rows": tuned["rows"] if tuned else None,
                        "l2": f"rotating buffers, {calls} x 2 MB per step > 126 MB L2",
                        "p10_us": round(per[len(per) // 10], 3),
@@ -413,6 +417,8 @@ def main():
     ap.add_argument("--impl", choices=["nvrar", "reference"], default="nvrar")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-autotune", action="store_true")
+    ap.add_argument("--no-multicast", action="store_true",
+                    help="do not set up the NVLS multicast one-shot candidate")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -89,7 +89,12 @@ typedef enum {
   /* virtual ranks sharing ONE device (nvrar_allreduce_local with every rank
    * present): no exchange — each unit is folded once, in the same order, from
    * all ranks' inputs and written to every rank's output. Elsewhere: HIER. */
-  NVRAR_ALGO_DIRECT = 4
+  NVRAR_ALGO_DIRECT = 4,
+  /* one-shot whose pushes go through an NVSwitch multicast (NVLS) mapping:
+   * one 16-byte multimem store per cell reaches every rank (egress M instead
+   * of (P-1)M). Needs nvrar_mc_attach; float32/bf16 with the
+   * Lamport protocol, messages up to 1 MB; otherwise runs ONESHOT. */
+  NVRAR_ALGO_MCAST = 5
 } nvrar_algo_t;
 
 /* Wire protocol. Both are self-validating (arrival of data = arrival of its
@@ -246,6 +251,19 @@ int nvrar_rd_inter(nvrar_comm_t comm, const uint64_t* packed, uint64_t* out, siz
 int nvrar_phase_local(nvrar_comm_t* comms, int ncomms, int phase, const void* const* send,
                       void* const* recv, size_t count, nvrar_dtype_t dtype, void* stream,
                       uint64_t active_mask);
+
+/* ---- NVLS multicast (optional; NVRAR_ALGO_MCAST) -------------------------
+ * The host supplies memory bound to an NVSwitch multicast object (torch
+ * symmetric memory, NCCL NVLS buffers, or its own cuMulticast* setup): the
+ * multicast mapping `mc_base` (a store reaches every rank's copy) and this
+ * rank's own mapping `local_base` of the same memory, at least
+ * nvrar_mc_bytes() bytes, at the same offset on every rank. Collective: every
+ * rank attaches before any rank selects NVRAR_ALGO_MCAST; the caller keeps the
+ * memory alive until nvrar_finalize. attach(comm, NULL, NULL, 0) detaches
+ * (when a peer failed to attach). */
+int nvrar_mc_bytes(nvrar_comm_t comm, size_t* bytes);
+int nvrar_mc_attach(nvrar_comm_t comm, void* mc_base, void* local_base, size_t bytes);
+int nvrar_mc_ready(nvrar_comm_t comm, int* ready);
 
 /* ---- config / introspection -------------------------------------------- */
 int nvrar_set_config(nvrar_comm_t comm, int blocks, uint64_t chunk_bytes);

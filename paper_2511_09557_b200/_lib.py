@@ -24,9 +24,9 @@ ERR_NOT_CONNECTED = 7
 
 INT32, FLOAT32, BF16 = 0, 1, 2
 SUM = 0
-ALGO_AUTO, ALGO_HIER, ALGO_TWOSHOT, ALGO_ONESHOT, ALGO_DIRECT = 0, 1, 2, 3, 4
+ALGO_AUTO, ALGO_HIER, ALGO_TWOSHOT, ALGO_ONESHOT, ALGO_DIRECT, ALGO_MCAST = 0, 1, 2, 3, 4, 5
 ALGO_NAMES = {ALGO_AUTO: "auto", ALGO_HIER: "hier", ALGO_TWOSHOT: "twoshot",
-              ALGO_ONESHOT: "oneshot", ALGO_DIRECT: "direct"}
+              ALGO_ONESHOT: "oneshot", ALGO_DIRECT: "direct", ALGO_MCAST: "mcast"}
 
 PROTO_AUTO, PROTO_LL, PROTO_LAMPORT = 0, 1, 2
 PROTO_CODES = {"auto": PROTO_AUTO, "ll": PROTO_LL, "lamport": PROTO_LAMPORT}
@@ -112,6 +112,9 @@ SIGNATURES = {
     "nvrar_rd_inter": (_c.c_int, [_vp, _vp, _vp, _c.c_size_t, _c.c_int, _vp]),
     "nvrar_phase_local": (_c.c_int, [_c.POINTER(_vp), _c.c_int, _c.c_int, _c.POINTER(_vp),
                                      _c.POINTER(_vp), _c.c_size_t, _c.c_int, _vp, _c.c_uint64]),
+    "nvrar_mc_bytes": (_c.c_int, [_vp, _c.POINTER(_c.c_size_t)]),
+    "nvrar_mc_attach": (_c.c_int, [_vp, _vp, _vp, _c.c_size_t]),
+    "nvrar_mc_ready": (_c.c_int, [_vp, _c.POINTER(_c.c_int)]),
     "nvrar_plan_local": (_c.c_int, [_c.POINTER(_vp), _c.c_int, _c.c_size_t, _c.c_int,
                                     _c.c_uint64, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
     "nvrar_plan_for": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_size_t, _c.c_int, _c.c_int,

@@ -172,7 +172,7 @@ class NvrarConfig:
 
 _DTYPES = {torch.float32: L.FLOAT32, torch.bfloat16: L.BF16, torch.int32: L.INT32}
 _ALGOS = {"auto": L.ALGO_AUTO, "hier": L.ALGO_HIER, "twoshot": L.ALGO_TWOSHOT,
-          "oneshot": L.ALGO_ONESHOT, "direct": L.ALGO_DIRECT}
+          "oneshot": L.ALGO_ONESHOT, "direct": L.ALGO_DIRECT, "mcast": L.ALGO_MCAST}
 
 
 def dtype_code(t: torch.dtype) -> int:
@@ -238,6 +238,51 @@ class Communicator:
         dist.all_gather_object(allh, mine, group=group)
         comm.connect(allh)  # type: ignore[arg-type]
         return comm
+
+    def enable_multicast(self, group=None) -> bool:
+        """Attach an NVLS multicast area from torch symmetric memory (the
+        plumbing: allocation + multicast rendezvous) so NVRAR_ALGO_MCAST can
+        run. Collective. Returns whether every rank has it; on any failure no
+        rank uses it."""
+        import torch.distributed as dist
+        ok = False
+        buf = None
+        nbytes = ctypes.c_size_t()
+        try:
+            import torch.distributed._symmetric_memory as symm
+            self._check(self._lib.nvrar_mc_bytes(self._h, ctypes.byref(nbytes)))
+            buf = symm.empty(nbytes.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+        except Exception as e:  # noqa: BLE001 — no multicast: the unicast schedules remain
+            self.mc_error = f"{type(e).__name__}: {e}"
+        # every rank enters the (collective) rendezvous, or none does
+        if not self._all_ok(buf is not None, group):
+            return False
+        try:
+            grp = group if group is not None else dist.group.WORLD
+            hdl = symm.rendezvous(buf, grp.group_name)
+            mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+            if mc:
+                ok = self._lib.nvrar_mc_attach(self._h, mc, buf.data_ptr(), nbytes.value) == 0
+            self._mc_keep = (buf, hdl)  # the memory must outlive the communicator's use
+        except Exception as e:  # noqa: BLE001
+            self.mc_error = f"{type(e).__name__}: {e}"
+        ok = self._all_ok(ok, group)
+        if not ok and self.multicast_ready():
+            self._check(self._lib.nvrar_mc_attach(self._h, None, None, 0))  # detach
+        return ok
+
+    def multicast_ready(self) -> bool:
+        r = ctypes.c_int()
+        self._check(self._lib.nvrar_mc_ready(self._h, ctypes.byref(r)))
+        return bool(r.value)
+
+    @staticmethod
+    def _all_ok(ok: bool, group) -> bool:
+        import torch.distributed as dist
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        return bool(t.item())
 
     # -- knobs / introspection --------------------------------------------------
     def set_config(self, cfg: NvrarConfig) -> None:

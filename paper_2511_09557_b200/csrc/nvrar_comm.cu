@@ -88,6 +88,7 @@ struct nvrar_comm {
   uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
   uint64_t* d_scratch = nullptr;
   std::vector<nvrar_plan_entry> table;  // measured selector (ascending max_bytes)
+  bool mc_ready = false;  // NVLS multicast area attached (nvrar_mc_attach)
 };
 
 namespace {
@@ -225,7 +226,10 @@ void plan_shape(int world, int nodes, int gpus, int algo_pref, int blocks_pref, 
   if (a == NVRAR_ALGO_AUTO) a = da;
   if (b <= 0) b = da == a ? db : std::max(db, 16);
   if ((a == NVRAR_ALGO_TWOSHOT || a == NVRAR_ALGO_ONESHOT) && !flat_ok) a = NVRAR_ALGO_HIER;
-  if (a == NVRAR_ALGO_ONESHOT && bytes > kOneshotMaxBytes) a = NVRAR_ALGO_TWOSHOT;
+  if ((a == NVRAR_ALGO_ONESHOT || a == NVRAR_ALGO_MCAST) && bytes > kOneshotMaxBytes) {
+    a = NVRAR_ALGO_TWOSHOT;
+  }
+  if (a == NVRAR_ALGO_MCAST && !flat_ok) a = NVRAR_ALGO_HIER;
   if (a == NVRAR_ALGO_DIRECT && !emu) a = NVRAR_ALGO_HIER;
   b = std::max(1, std::min(b, max_ctas));
   *algo = a;
@@ -466,10 +470,13 @@ int nvrar_init(const nvrar_init_args* a, nvrar_comm_t* out) {
   return NVRAR_SUCCESS;
 }
 
+static void mc_teardown(nvrar_comm* c);
+
 int nvrar_finalize(nvrar_comm_t c) {
   if (!c) return NVRAR_SUCCESS;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  mc_teardown(c);
   for (auto* p : c->opened) cudaIpcCloseMemHandle(p);
   for (auto* p : c->sym_allocs) cudaFree(p);
   if (c->region) cudaFree(c->region);
@@ -505,7 +512,7 @@ int nvrar_set_config(nvrar_comm_t c, int blocks, uint64_t chunk_bytes) {
 }
 
 int nvrar_set_algo(nvrar_comm_t c, nvrar_algo_t algo) {
-  if (!c || algo < NVRAR_ALGO_AUTO || algo > NVRAR_ALGO_DIRECT) {
+  if (!c || algo < NVRAR_ALGO_AUTO || algo > NVRAR_ALGO_MCAST) {
     return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad algo");
   }
   if ((algo == NVRAR_ALGO_TWOSHOT || algo == NVRAR_ALGO_ONESHOT) &&
@@ -559,7 +566,8 @@ int nvrar_set_plan_table(nvrar_comm_t c, const nvrar_plan_entry* entries, int n)
   if (!c || n < 0 || (n > 0 && !entries)) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad table");
   std::vector<nvrar_plan_entry> t(entries, entries + n);
   for (int i = 0; i < n; ++i) {
-    if (t[i].algo < NVRAR_ALGO_HIER || t[i].algo > NVRAR_ALGO_ONESHOT || t[i].blocks < 1 ||
+    if (t[i].algo < NVRAR_ALGO_HIER || t[i].algo > NVRAR_ALGO_MCAST ||
+        t[i].algo == NVRAR_ALGO_DIRECT || t[i].blocks < 1 ||
         (i > 0 && t[i].max_bytes <= t[i - 1].max_bytes)) {
       return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
                   "plan table entry %d: need ascending max_bytes, a concrete algo, blocks >= 1", i);
@@ -702,6 +710,16 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
     algo = NVRAR_ALGO_HIER;
     if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   }
+  const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
+  // one-shot over NVLS multicast: a single real rank with the multicast area
+  // bound; anything else runs the unicast one-shot (same bits either way)
+  bool mc = false;
+  if (algo == NVRAR_ALGO_MCAST) {
+    mc = !emu && nl == 1 && c0->mc_ready && lamport && phase == NVRAR_PHASE_ALL &&
+         count * dtype_bytes(dtype) <= kOneshotMaxBytes;
+    algo = NVRAR_ALGO_ONESHOT;
+  }
+  lp.mc = mc ? 1 : 0;
   if (order != NVRAR_ORDER_NVRAR && algo != NVRAR_ALGO_ONESHOT && algo != NVRAR_ALGO_TWOSHOT) {
     // the ring / tree orders exist on the flat schedules only
     algo = count * dtype_bytes(dtype) <= (c0->world <= 4 ? (1u << 20) : (256u << 10)) &&
@@ -722,7 +740,6 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   // by value: the kernel reads it from param space (EMU: only the topology fields
   // are shared by the virtual ranks; each reads the rest through desc[])
   lp.d0 = c0->h_desc;
-  const bool lamport = dtype != NVRAR_INT32 && c0->proto != NVRAR_PROTO_LL;
   KernelFn k = phase != NVRAR_PHASE_ALL ? select_phase(dtype, phase, c0->nodes, emu)
                : direct ? select_direct(dtype, c0->nodes, c0->gpus)
                         : select_kernel(dtype, algo != NVRAR_ALGO_HIER,
@@ -1002,3 +1019,52 @@ int nvrar_check(nvrar_comm_t c) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// NVLS multicast area (NVRAR_ALGO_MCAST). The host framework supplies a
+// multicast mapping and this rank's own mapping of the same memory (e.g.
+// torch symmetric memory, NCCL's NVLS buffers); the library only uses them.
+static void mc_teardown(nvrar_comm* c) {
+  c->mc_ready = false;
+  c->h_desc.mc = nullptr;
+  c->h_desc.mc_local = nullptr;
+}
+
+int nvrar_mc_bytes(nvrar_comm_t c, size_t* bytes) {
+  if (!c || !bytes) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  *bytes = 2ull * c->world * c->lay.a_src * 8;  // [2 parity][P src][a_src words]
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_mc_attach(nvrar_comm_t c, void* mc_base, void* local_base, size_t bytes) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  if (!c->connected) return fail(c, NVRAR_ERR_NOT_CONNECTED, "comm not connected");
+  if (!mc_base && !local_base && bytes == 0) {  // detach (a peer failed to attach)
+    mc_teardown(c);
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpy(c->d_desc, &c->h_desc, sizeof(RankDesc), cudaMemcpyHostToDevice));
+    return NVRAR_SUCCESS;
+  }
+  size_t need = 0;
+  nvrar_mc_bytes(c, &need);
+  if (!mc_base || !local_base || bytes < need ||
+      (reinterpret_cast<uintptr_t>(mc_base) | reinterpret_cast<uintptr_t>(local_base)) & 15u) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                "multicast area: need %zu bytes, 16-byte aligned mappings", need);
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  // every cell starts empty (the Lamport invariant), like the region
+  CUDA_TRY(c, cudaMemset(local_base, 0xFF, need));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  c->h_desc.mc = static_cast<uint8_t*>(mc_base);
+  c->h_desc.mc_local = static_cast<uint8_t*>(local_base);
+  CUDA_TRY(c, cudaMemcpy(c->d_desc, &c->h_desc, sizeof(RankDesc), cudaMemcpyHostToDevice));
+  c->mc_ready = true;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_mc_ready(nvrar_comm_t c, int* ready) {
+  if (!c || !ready) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  *ready = c->mc_ready ? 1 : 0;
+  return NVRAR_SUCCESS;
+}

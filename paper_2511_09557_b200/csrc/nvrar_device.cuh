@@ -90,6 +90,12 @@ struct RankDesc {
   int profile;
   uint32_t poll_ns;  // back-off between unsatisfied polls (0 = spin)
   uint64_t timeout_ns;
+  // NVLS multicast A area (one-shot over multicast): the multicast mapping
+  // (stores reach every rank's copy) and this rank's own copy; same
+  // [2 parity][P src][a_src words] shape as the region's A slots. Null when
+  // multicast is not set up.
+  uint8_t* mc;
+  uint8_t* mc_local;
 };
 
 // One rank per launch (the real multi-GPU path) passes its descriptor BY VALUE
@@ -109,6 +115,7 @@ struct LaunchParams {
   // with the element type's own add (bf16: fp32 add of the rounded sum, one
   // RNE) — bit-identical to the all-reduce followed by `resid + out`
   const void* resid[kMaxLocal];
+  int mc;  // flat one-shot: push each unit once through the multicast mapping
 };
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):
@@ -147,6 +154,15 @@ __device__ __forceinline__ uint4 ld_volatile16(const void* p) {
 #ifndef NVRAR_PUT_ST
 #define NVRAR_PUT_ST "st.volatile.global.v4.u32"
 #endif
+// One 16-byte store to a multicast (NVLS) address: the NVSwitch replicates it
+// into every member GPU's copy of the line. The payload is raw bits.
+__device__ __forceinline__ void st_mc16(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "f"(__uint_as_float(a)), "f"(__uint_as_float(b)), "f"(__uint_as_float(c)),
+               "f"(__uint_as_float(d))
+               : "memory");
+}
+
 __device__ __forceinline__ void st_volatile16(void* p, uint32_t a, uint32_t b, uint32_t c,
                                               uint32_t d) {
   asm volatile(NVRAR_PUT_ST " [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d));
@@ -265,6 +281,14 @@ struct LL {
     }
   }
   template <int W>
+  __device__ static __forceinline__ void put_mc(uint4* slot, uint64_t u, const uint32_t (&d)[W],
+                                                uint32_t seq) {
+#pragma unroll
+    for (int h = 0; h < W / 2; ++h) {
+      st_mc16(slot + cell_index(u, W / 2, h), d[2 * h], seq, d[2 * h + 1], seq);
+    }
+  }
+  template <int W>
   __device__ static __forceinline__ bool try_get(const uint4* slot, uint64_t u, uint32_t seq,
                                                  uint32_t (&d)[W], uint32_t& bad) {
     bool ok = true;
@@ -324,6 +348,15 @@ struct Lamport {
     for (int h = 0; h < W / 4; ++h) {
       st_volatile16(slot + cell_index(u, W / 4, h), canon(d[4 * h]), canon(d[4 * h + 1]),
                     canon(d[4 * h + 2]), canon(d[4 * h + 3]));
+    }
+  }
+  template <int W>
+  __device__ static __forceinline__ void put_mc(uint4* slot, uint64_t u, const uint32_t (&d)[W],
+                                                uint32_t) {
+#pragma unroll
+    for (int h = 0; h < W / 4; ++h) {
+      st_mc16(slot + cell_index(u, W / 4, h), canon(d[4 * h]), canon(d[4 * h + 1]),
+              canon(d[4 * h + 2]), canon(d[4 * h + 3]));
     }
   }
   template <int W>

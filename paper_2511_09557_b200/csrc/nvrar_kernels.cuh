@@ -554,9 +554,25 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   }
 
   // Reduce-scatter pushes: the owner q of each sub-shard receives our copy.
+  // Multicast one-shot: ONE store per cell to the multicast mapping reaches
+  // slot `me` of every rank's multicast A area (the NVSwitch replicates it).
+  const bool mc = lp.mc != 0;
+  uint4* const mc_slot = mc ? reinterpret_cast<uint4*>(
+                                  d.mc + (static_cast<uint64_t>(parity) * d.world + me) * d.lay.a_src * 8)
+                            : nullptr;
+  if (mc) {
+    if (pv[0] > 0) Raw::template put_mc<RDW>(mc_slot, u_first, pre[0], c.seq);
+    for (uint64_t u = u_first + blockDim.x; u < ue; u += blockDim.x) {
+      const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(UE * u));
+      if (valid == 0) continue;
+      uint32_t raw[RDW];
+      load_raw<E, UE>(send, UE * u, valid, raw);
+      Raw::template put_mc<RDW>(mc_slot, u, raw, c.seq);
+    }
+  }
 #pragma unroll
   for (int j = 1; j < kPre; ++j) {
-    if (j < P) {
+    if (j < P && !mc) {
       // compile-time indices only (a runtime index would put pre[] in local memory)
       if (oneshot) {
         if (pv[0] > 0) Raw::template put<RDW>(slot_a(d, (me + j) % P, parity, me), u_first, pre[0], c.seq);
@@ -565,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       }
     }
   }
-  for (int j = 1; j < P; ++j) {
+  for (int j = 1; j < (mc ? 1 : P); ++j) {
     const int q = (me + j) % P;
     const uint64_t qbase = oneshot ? 0 : static_cast<uint64_t>(q) * SP;
     uint4* slot = slot_a(d, q, parity, me);
@@ -597,7 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   // unit's first element) and walks the fold order incrementally.
   const uint32_t mybase = oneshot ? 0u : static_cast<uint32_t>(me * SP);
   const uint32_t n32 = static_cast<uint32_t>(n), SG32 = static_cast<uint32_t>(SG);
-  uint8_t* const a_mine = d.base[me] + d.lay.a_off + static_cast<uint64_t>(parity) * d.world * d.lay.a_src * 8;
+  uint8_t* const a_mine = (mc ? d.mc_local : d.base[me] + d.lay.a_off) +
+                          static_cast<uint64_t>(parity) * d.world * d.lay.a_src * 8;
   const uint64_t a_stride = d.lay.a_src * 8;
   for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
     const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);

@@ -24,7 +24,8 @@ from . import dist as D
 from .comm import Communicator, NvrarConfig
 
 DEFAULT_SIZES = (64 << 10, 128 << 10, 256 << 10, 512 << 10, 1 << 20, 2 << 20, 4 << 20, 8 << 20)
-ALGO_CODE = {"hier": L.ALGO_HIER, "twoshot": L.ALGO_TWOSHOT, "oneshot": L.ALGO_ONESHOT}
+ALGO_CODE = {"hier": L.ALGO_HIER, "twoshot": L.ALGO_TWOSHOT, "oneshot": L.ALGO_ONESHOT,
+             "mcast": L.ALGO_MCAST}
 
 
 def _graph(fn, calls, stream):
@@ -103,12 +104,16 @@ def autotune(comm: Communicator, sizes: Sequence[int] = DEFAULT_SIZES,
     measured: Dict[int, Dict[str, float]] = {}
     best: Dict[int, Tuple[str, int, float]] = {}
     flat_ok = comm.topo.world_size() <= 16
+    # the multicast one-shot is a candidate only where every rank set it up
+    mcast = comm.multicast_ready() and dtype != torch.int32
     for size in sizes:
         row: Dict[str, float] = {}
-        for algo in ("oneshot", "hier", "twoshot"):
+        for algo in ("oneshot", "mcast", "hier", "twoshot"):
             if algo != "hier" and not flat_ok:
                 continue
-            if algo == "oneshot" and size > (1 << 20):
+            if algo in ("oneshot", "mcast") and size > (1 << 20):
+                continue
+            if algo == "mcast" and not mcast:
                 continue
             for b in blocks:
                 row[f"{algo}/{b}"] = measure(comm, size, dtype, algo, b, calls, reps, group)

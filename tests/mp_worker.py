@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--nodes", type=int, required=True)
     ap.add_argument("--gpus", type=int, required=True)
     ap.add_argument("--mismatch", action="store_true", help="length-mismatch protocol fault")
+    ap.add_argument("--multicast", action="store_true", help="also test the NVLS one-shot")
     ap.add_argument("--ag-mismatch", action="store_true",
                     help="all-gather shard-length mismatch (collectives_test.cpp:226-237)")
     args = ap.parse_args()
@@ -150,6 +151,37 @@ def main():
             if not np.array_equal(got, want):
                 fails += 1
                 print(f"rank {rank}: {order} {dtype} differs", flush=True)
+
+    # NVLS multicast one-shot: same bits as every other schedule
+    if args.multicast:
+        mc = comm.enable_multicast()
+        print(f"rank {rank}: multicast ready={mc} {getattr(comm, 'mc_error', '')}", flush=True)
+        if mc:
+            comm.set_algo("mcast")
+            for dtype in ("f32", "bf16", "i32"):
+                for n in (1, 1031, 65539, 262144):
+                    x = inputs(dtype, world, n, 970 + n)
+                    if dtype == "f32" and n > 1:
+                        x.view(np.uint32)[1, 1] = 0xFFFFFFFF  # the Lamport empty pattern as data
+                    want = O.nvrar_order_sum(x, args.nodes, args.gpus, dtype)
+                    inp = to_dev(x[rank], dtype)
+                    out = torch.empty_like(inp)
+                    for _ in range(3):  # both parities
+                        comm.allreduce(inp, out)
+                    torch.cuda.synchronize()
+                    comm.check()
+                    got = from_dev(out, dtype)
+                    if dtype == "f32":
+                        ok = np.array_equal(np.isnan(got), np.isnan(want)) and np.array_equal(
+                            got[~np.isnan(got)].view(np.uint32), want[~np.isnan(want)].view(np.uint32))
+                    else:
+                        ok = np.array_equal(got, want)
+                    if not ok:
+                        fails += 1
+                        print(f"rank {rank}: mcast {dtype} n={n} differs", flush=True)
+            comm.set_algo("auto")
+        elif world > 1:
+            fails += 1
 
     algos = ["hier", "twoshot", "oneshot"]
     for dtype in ("f32", "bf16", "i32"):

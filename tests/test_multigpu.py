@@ -62,3 +62,13 @@ def test_all_gather_length_mismatch_is_protocol_fault():
     rc, out = _run(2, 1, 2, ("--ag-mismatch",))
     assert rc == 0, out[-4000:]
     assert out.count("ag mismatch status 4") == 2, out[-4000:]
+
+
+@pytest.mark.parametrize("world,nodes,gpus", [(2, 2, 1), (4, 2, 2), (4, 1, 4), (8, 2, 4)])
+def test_multicast_oneshot_parity(world, nodes, gpus):
+    """NVLS multicast one-shot (NVRAR_ALGO_MCAST) is bit-exact like every schedule."""
+    if NDEV < world:
+        pytest.skip(f"needs {world} GPUs, have {NDEV}")
+    rc, out = _run(world, nodes, gpus, ("--multicast",))
+    assert rc == 0, out[-4000:]
+    assert out.count(": OK") == world, out[-4000:]
