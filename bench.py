@@ -383,6 +383,13 @@ def run_multi(args, rank, world, local):
                        "selector": "autotuned on this box" if tuned else "built-in policy",
                        "multicast": mc_ok,
                        "selector_rows": tuned["rows"] if tuned else None,
+                       # alpha-beta model fitted to this run
+                       "alpha_beta": dict(S.fit_schedules(tuned["measured"]) if tuned else {},
+                                          nccl=dict(zip(("alpha_us", "beta_GBs"), [
+                                              round(v, 3) for v in S.fit_alpha_beta(
+                                                  {int(k[:-2]) << 10: r["nccl_us"]
+                                                   for k, r in sweep.items()})])) if sweep
+                                          else None),
                        "l2": f"rotating buffers, {calls} x 2 MB per step > 126 MB L2",
                        "p10_us": round(per[len(per) // 10], 3),
                        "p90_us": round(per[(9 * len(per)) // 10], 3),

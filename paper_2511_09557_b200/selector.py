@@ -125,6 +125,43 @@ def autotune(comm: Communicator, sizes: Sequence[int] = DEFAULT_SIZES,
     return {"rows": rows, "measured": measured}
 
 
+def fit_alpha_beta(points: Dict[int, float]) -> Tuple[float, float]:
+    """Least-squares fit of the alpha-beta cost model t(M) = alpha + M / beta
+    (cost_model.hpp's per-algorithm form, ModelPrediction::of) to measured
+    (bytes, µs) points. Returns (alpha_us, beta_GBs); beta is inf when the
+    points show no size dependence."""
+    xs = [float(m) for m in points]
+    ys = [float(points[m]) for m in points]
+    n = len(xs)
+    if n == 0:
+        raise ValueError("no points")
+    if n == 1:
+        return ys[0], math.inf
+    mx, my = sum(xs) / n, sum(ys) / n
+    sxx = sum((x - mx) ** 2 for x in xs)
+    slope = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sxx if sxx else 0.0
+    alpha = my - slope * mx
+    beta = math.inf if slope <= 0 else 1.0 / slope / 1e3  # bytes/µs -> GB/s
+    return alpha, beta
+
+
+def fit_schedules(measured: Dict[int, Dict[str, float]]) -> Dict[str, dict]:
+    """alpha/beta per schedule from autotune()'s measurements (best CTA count
+    per size)."""
+    per: Dict[str, Dict[int, float]] = {}
+    for size, cands in measured.items():
+        for k, t in cands.items():
+            algo = k.split("/")[0]
+            per.setdefault(algo, {})
+            per[algo][size] = min(t, per[algo].get(size, math.inf))
+    out = {}
+    for algo, pts in per.items():
+        a, b = fit_alpha_beta(pts)
+        out[algo] = {"alpha_us": round(a, 3), "beta_GBs": None if math.isinf(b) else round(b, 1),
+                     "sizes": sorted(pts)}
+    return out
+
+
 def save(path: str, result: dict) -> None:
     with open(path, "w") as fh:
         json.dump({"rows": result["rows"]}, fh)

@@ -59,3 +59,14 @@ def test_gloo_world2_host_logic():
     for p in ps:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_alpha_beta_fit():
+    """selector.fit_alpha_beta recovers t = alpha + M / beta exactly."""
+    from paper_2511_09557_b200.selector import fit_alpha_beta, fit_schedules
+    pts = {m: 5.0 + m / (400.0 * 1e3) for m in (65536, 262144, 1 << 20, 4 << 20)}
+    a, b = fit_alpha_beta(pts)
+    assert abs(a - 5.0) < 1e-9 and abs(b - 400.0) < 1e-6
+    fs = fit_schedules({65536: {"oneshot/32": 5.2, "oneshot/64": 5.1, "hier/32": 7.0},
+                        1 << 20: {"oneshot/32": 9.0, "hier/32": 9.5}})
+    assert set(fs) == {"oneshot", "hier"} and fs["oneshot"]["beta_GBs"] > 0
