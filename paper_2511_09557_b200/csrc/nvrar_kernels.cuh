@@ -76,19 +76,16 @@ __device__ __forceinline__ void begin_wait(const RankDesc& d) {
   stamp(d, 7);
 }
 
-#ifndef NVRAR_SEQ_LD
-#define NVRAR_SEQ_LD "ld.volatile.global.u32"
-#endif
 // The call number and the sticky fault word of this CTA (thread 0 only). Only
-// this GPU's kernels write them.
+// this GPU's kernels write them (a gpu-scope load measured no faster).
 struct SeqWords {
   uint32_t err, seq;
 };
 __device__ __forceinline__ SeqWords seq_issue(const RankDesc& d) {
   SeqWords w{0u, 0u};
   if (threadIdx.x == 0) {
-    asm volatile(NVRAR_SEQ_LD " %0, [%1];" : "=r"(w.err) : "l"(&d.state->err.code));
-    asm volatile(NVRAR_SEQ_LD " %0, [%1];" : "=r"(w.seq) : "l"(&d.state->seq[blockIdx.x]));
+    w.err = ld_volatile32(&d.state->err.code);
+    w.seq = ld_volatile32(&d.state->seq[blockIdx.x]);
   }
   return w;
 }
@@ -595,9 +592,6 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       Raw::template put<RDW>(slot, u, raw, c.seq);
     }
   }
-#ifdef NVRAR_PUSH_FENCE
-  __threadfence_system();  // experiment: push the remote stores out now
-#endif
   stamp(d, 2);
   c.phase = 3;
 
