@@ -1,12 +1,12 @@
 """NVRAR all-reduce benchmark (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nvrar|reference]
-                    [--no-sweep] [--no-autotune]
+                    [--no-sweep] [--no-autotune] [--no-multicast]
 
 N=1  : BASELINE configs[0] on one B200 — 8 ranks as 2 virtual nodes x 4, 1 MB
-       fp32 sum; the 8 ranks are virtual ranks on cuda:0 (one cooperative
-       launch, all ranks' buffers in one HBM), the GPU analogue of the
-       reference running all ranks in one process.
+       fp32 sum; the 8 ranks are virtual ranks on cuda:0 (one launch for all
+       ranks, every buffer in one HBM — the direct schedule), the GPU analogue
+       of the reference running all ranks in one process.
 N>1  : launched by torch.distributed.run, one rank per GPU; hierarchy 2 x N/2
        (N=8: 2x4, configs[1]); headline message 1 MB bf16, plus the 64 KB-8 MB
        sweep against NCCL all-reduce on the same buffers (configs[1]/[2]).
@@ -234,7 +234,7 @@ def run_emulated(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (oracles::random_inputs, seed 1234); output checked bit-exact vs oracle",
         "config": {"workload": "configs[0]: 2x4 virtual nodes (8 ranks as virtual ranks on one "
-                               "B200, one cooperative launch per all-reduce), 1 MB fp32 sum",
+                               "B200, one launch per all-reduce), 1 MB fp32 sum",
                    "nodes": nodes, "gpus_per_node": gpus, "message_bytes": msg, "algo": algo,
                    "blocks_per_rank": blocks, "calls_per_step": calls,
                    "per_schedule_us": by_algo,
