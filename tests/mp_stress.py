@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--nodes", type=int, default=2)
     ap.add_argument("--graph", action="store_true", help="capture runs of calls in CUDA graphs")
     ap.add_argument("--sync-every", type=int, default=1)
+    ap.add_argument("--multicast", action="store_true", help="also the NVLS one-shot")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -38,6 +39,13 @@ def main():
     rng = random.Random(1234)
     sizes = [1, 7, 1000, 4099, 65536, 131072, 300001, 1 << 20]
     algos = ["hier", "twoshot", "oneshot", "auto"]
+    if args.multicast:
+        if not comm.enable_multicast():
+            print(f"rank {rank}: multicast unavailable: {getattr(comm, 'mc_error', '')}", flush=True)
+        else:
+            algos.append("mcast")
+    # call kinds: the all-reduce, its fused residual epilogue, the ring / tree orders
+    kinds = ["allreduce", "allreduce", "residual", "ring", "tree"]
     dtypes = [torch.bfloat16, torch.float32, torch.int32]
     total = world * (world + 1) // 2
     bad = 0
@@ -49,13 +57,25 @@ def main():
         n = rng.choice(sizes)
         if dt != torch.int32 and n > (1 << 20) // 2:
             n = (1 << 20) // 2
+        kind = rng.choice(kinds)
+        if kind == "ring" and world > 8:
+            kind = "allreduce"
         comm.set_algo(algo)
         comm.set_config(NvrarConfig(blocks, 65536))
         idx = torch.arange(n, device="cuda", dtype=torch.int64) % 7 + 1
         x = (idx * (rank + 1)).to(dt)
         y = torch.empty_like(x)
-        comm.allreduce(x, y)
-        pending.append((it, algo, blocks, dt, n, idx, y))
+        resid = None
+        if kind == "residual":
+            resid = idx.to(dt)
+            comm.allreduce_residual(x, resid, out=y)
+        elif kind == "ring":
+            comm.ring_allreduce(x, y)
+        elif kind == "tree":
+            comm.tree_allreduce(x, y)
+        else:
+            comm.allreduce(x, y)
+        pending.append((it, f"{kind}:{algo}", blocks, dt, n, idx, y, resid))
         if (it + 1) % args.sync_every == 0 or it == args.calls - 1:
             torch.cuda.synchronize()
             rc = comm.check_status()
@@ -63,8 +83,10 @@ def main():
                 print(f"rank {rank}: call {it} status {rc}: {comm.last_error()}", flush=True)
                 bad += 1
                 break
-            for (i, a, b, d, nn, ix, yy) in pending:
+            for (i, a, b, d, nn, ix, yy, rr) in pending:
                 want = (ix * total).to(d)
+                if rr is not None:
+                    want = want + rr  # the element type's own add, like the kernel
                 if not torch.equal(yy, want):
                     nbad = int((yy != want).sum())
                     print(f"rank {rank}: call {i} {a}/{b} {d} n={nn}: {nbad} wrong", flush=True)

@@ -72,3 +72,20 @@ def test_multicast_oneshot_parity(world, nodes, gpus):
     rc, out = _run(world, nodes, gpus, ("--multicast",))
     assert rc == 0, out[-4000:]
     assert out.count(": OK") == world, out[-4000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_mixed_call_stress(world):
+    """Hundreds of back-to-back calls switching schedule (incl. the multicast
+    one-shot), CTA count, dtype, size and call kind (all-reduce, fused
+    residual, ring / tree orders) — every result checked (tests/mp_stress.py)."""
+    if NDEV < world:
+        pytest.skip(f"needs {world} GPUs, have {NDEV}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tests", "mp_stress.py"),
+           "--calls", "600", "--multicast", "--sync-every", "7"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count(": OK after 600 calls") == world, out[-4000:]
