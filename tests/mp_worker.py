@@ -43,16 +43,50 @@ def inputs(dtype, p, n, seed):
     return O.bf16_bits_from_f32(x) if dtype == "bf16" else x
 
 
+def parity_loop(comm, args, rank, world, sizes):
+    """Every schedule x dtype against the oracle's bits; returns the failures."""
+    fails = 0
+    for dtype in ("f32", "bf16", "i32"):
+        for algo in ("hier", "twoshot", "oneshot"):
+            comm.set_algo(algo)
+            for n in sizes:
+                x = inputs(dtype, world, n, 1000 + n)
+                want = O.nvrar_order_sum(x, args.nodes, args.gpus,
+                                         {"f32": "f32", "bf16": "bf16", "i32": "i32"}[dtype])
+                inp = to_dev(x[rank], dtype)
+                out = torch.empty_like(inp)
+                plan = D.plan_consensus(comm.plan(n, inp.dtype))
+                comm.allreduce(inp, out)
+                torch.cuda.synchronize()
+                comm.check()
+                got = from_dev(out, dtype)
+                if dtype == "f32":
+                    got, want = got.view(np.uint32), want.view(np.uint32)
+                bad = int(np.count_nonzero(got != want))
+                if bad:
+                    fails += 1
+                    print(f"rank {rank}: {dtype} {algo} {plan} n={n}: {bad} mismatches", flush=True)
+    comm.set_algo("auto")
+    return fails
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nodes", type=int, required=True)
     ap.add_argument("--gpus", type=int, required=True)
     ap.add_argument("--mismatch", action="store_true", help="length-mismatch protocol fault")
     ap.add_argument("--multicast", action="store_true", help="also test the NVLS one-shot")
+    ap.add_argument("--dev-mod", type=int, default=0, help="device = LOCAL_RANK %% dev_mod")
+    ap.add_argument("--quick", action="store_true", help="only the schedule x dtype parity loop")
     ap.add_argument("--ag-mismatch", action="store_true",
                     help="all-gather shard-length mismatch (collectives_test.cpp:226-237)")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
+    if args.dev_mod:
+        # more ranks than GPUs (e.g. the 8-rank layout on 4 GPUs): two processes
+        # share a device and progress by time-slicing — a slow but complete run
+        # of the P=8 kernel instantiations
+        local = local % args.dev_mod
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -79,6 +113,14 @@ def main():
         print(f"rank {rank}: ag mismatch status {rc} ({comm.last_error()})", flush=True)
         dist.barrier()
         sys.exit(0 if rc == L.ERR_PROTOCOL_FAULT else 1)
+
+    if args.quick:
+        fails += parity_loop(comm, args, rank, world, (1031, 65539))
+        print(f"rank {rank}: {'OK' if fails == 0 else f'{fails} FAILURES'}", flush=True)
+        dist.barrier()
+        comm.close()
+        dist.destroy_process_group()
+        sys.exit(1 if fails else 0)
 
     # the phase-only entry points across processes (nvrar.h phase section)
     G = args.gpus
@@ -183,27 +225,7 @@ def main():
         elif world > 1:
             fails += 1
 
-    algos = ["hier", "twoshot", "oneshot"]
-    for dtype in ("f32", "bf16", "i32"):
-        for algo in algos:
-            comm.set_algo(algo)
-            for n in (1, 1031, 65539, 262144):
-                x = inputs(dtype, world, n, 1000 + n)
-                want = O.nvrar_order_sum(x, args.nodes, args.gpus,
-                                         {"f32": "f32", "bf16": "bf16", "i32": "i32"}[dtype])
-                inp = to_dev(x[rank], dtype)
-                out = torch.empty_like(inp)
-                plan = D.plan_consensus(comm.plan(n, inp.dtype))
-                comm.allreduce(inp, out)
-                torch.cuda.synchronize()
-                comm.check()
-                got = from_dev(out, dtype)
-                if dtype == "f32":
-                    got, want = got.view(np.uint32), want.view(np.uint32)
-                bad = int(np.count_nonzero(got != want))
-                if bad:
-                    fails += 1
-                    print(f"rank {rank}: {dtype} {algo} {plan} n={n}: {bad} mismatches", flush=True)
+    fails += parity_loop(comm, args, rank, world, (1, 1031, 65539, 262144))
     # back-to-back calls captured in a CUDA graph, replayed (seq lives on the device)
     comm.set_algo("auto")
     comm.set_config(NvrarConfig())
