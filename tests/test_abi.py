@@ -102,3 +102,21 @@ def test_deadlock_error_formats_blocked_set():
                          C.BlockedRank(1, C.BlockedRank.Kind.SeqWait, peer_rank=3, expected=2)])
     assert "2 rank(s) blocked" in str(e)
     assert e.blocked()[1].peer_rank == 3
+
+
+def test_selector_default_policy_and_fallbacks():
+    """The built-in policy (nvrar_comm.cu default_plan) and the schedule fallbacks."""
+    # one-shot while (P-1)M inbound stays small; two-shot above it at P <= 4
+    assert plan_for(4, 2, 2, (256 << 10) // 2, L.BF16)[0] == "oneshot"
+    assert plan_for(4, 2, 2, (2 << 20) // 2, L.BF16)[0] == "twoshot"
+    # the paper's hierarchy in the middle at P = 8
+    assert plan_for(8, 2, 4, (1 << 20) // 2, L.BF16)[0] == "hier"
+    assert plan_for(8, 2, 4, (8 << 20) // 2, L.BF16)[0] == "twoshot"
+    # single rank: a copy through the one-shot
+    assert plan_for(1, 1, 1, 1000, L.FLOAT32)[0] == "oneshot"
+    # multicast one-shot: bounded like the one-shot; hierarchy where flat is not allowed
+    assert plan_for(4, 2, 2, 1000, L.BF16, algo=L.ALGO_MCAST)[0] == "mcast"
+    assert plan_for(4, 2, 2, (4 << 20) // 2, L.BF16, algo=L.ALGO_MCAST)[0] == "twoshot"
+    assert plan_for(32, 8, 4, 1000, L.BF16, algo=L.ALGO_MCAST)[0] == "hier"
+    # the direct schedule exists only for a local group of virtual ranks
+    assert plan_for(8, 2, 4, 1000, L.FLOAT32, algo=L.ALGO_DIRECT)[0] == "hier"
