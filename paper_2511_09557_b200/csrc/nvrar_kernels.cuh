@@ -578,7 +578,25 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       }
     }
   }
-  for (int j = 1; j < (mc ? 1 : P); ++j) {
+  if (oneshot && !mc) {
+    // one-shot: the same unit goes to every peer — load it once, store P-1 times
+    for (uint64_t u = u_first + blockDim.x; u < ue; u += blockDim.x) {
+      const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(UE * u));
+      if (valid == 0) continue;
+      uint32_t raw[RDW];
+      load_raw<E, UE>(send, UE * u, valid, raw);
+      int q = me;
+      for (int j = 1; j < P; ++j) {
+        q = q + 1 == P ? 0 : q + 1;
+        Raw::template put<RDW>(slot_a(d, q, parity, me), u, raw, c.seq);
+      }
+    }
+    // peers beyond the prefetch loop's reach have not had the first unit yet
+    for (int j = kPre; j < P; ++j) {
+      if (pv[0] > 0) Raw::template put<RDW>(slot_a(d, (me + j) % P, parity, me), u_first, pre[0], c.seq);
+    }
+  }
+  for (int j = 1; j < (mc || oneshot ? 1 : P); ++j) {
     const int q = (me + j) % P;
     const uint64_t qbase = oneshot ? 0 : static_cast<uint64_t>(q) * SP;
     uint4* slot = slot_a(d, q, parity, me);
