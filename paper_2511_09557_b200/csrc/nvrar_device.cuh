@@ -687,6 +687,15 @@ __device__ __forceinline__ void stamp(const RankDesc& d, int k) {
   if (d.profile && threadIdx.x == 0) d.state->ts[blockIdx.x][k] = globaltimer();
 }
 
+// Pull the residual unit of element e into L2 while the unit's data is still
+// in flight (no registers held; emit's load then hits L2).
+template <class E>
+__device__ __forceinline__ void prefetch_resid(const void* resid, uint64_t e) {
+  if (resid != nullptr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(resid) + e * E::kBytes));
+  }
+}
+
 // Final store of an output unit: plain, or fused with the residual add.
 template <class E, int UE>
 __device__ __forceinline__ void emit(void* recv, const void* resid, uint64_t e, int valid,

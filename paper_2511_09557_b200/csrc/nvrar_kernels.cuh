@@ -296,6 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
       uu[k] = u0 + static_cast<uint64_t>(k) * blockDim.x;
       valid[k] = uu[k] < ue ? chunk_valid<UE>(S, uu[k], n, mybase) : 0;
     }
+#pragma unroll
+    for (int k = 0; k < kHierUpt; ++k) {
+      if (kFull && valid[k] > 0) prefetch_resid<E>(resid, mybase + UE * uu[k]);
+    }
     if constexpr (kRD) {
       // rd_inter input: this rank's shard packed as LL words {data, seq}; every
       // flag must be this call's (nvrar.hpp:145-150); one node copies (:140-143)
@@ -456,7 +460,10 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
         valid[j - 1] = 0;
         if (j < G) {
           valid[j - 1] = chunk_valid<UE>(S, u, n, static_cast<uint64_t>(s) * S);
-          if (valid[j - 1] > 0) pending |= 1u << (j - 1);
+          if (valid[j - 1] > 0) {
+            pending |= 1u << (j - 1);
+            prefetch_resid<E>(resid, static_cast<uint64_t>(s) * S + UE * u);
+          }
         }
       }
       recv_grid<Raw, RDW, 1, MG - 1>(c, slots, u, r, pending, peers);
@@ -632,6 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
     if (valid == 0) continue;
+    prefetch_resid<E>(resid, e0);
     const bool tree = order == kOrderTree;
     // the tree chain does not depend on the chunk: one fixed order
     const int c0 = tree ? 0 : static_cast<int>(e0 / SG32);
@@ -757,7 +765,10 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
             slots[0][t] = reinterpret_cast<uint4*>(b_mine + static_cast<uint64_t>(q) * b_stride);
             const uint32_t e0 = static_cast<uint32_t>(q * SP) + UE * static_cast<uint32_t>(u);
             valid[t] = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
-            if (valid[t] > 0) pending |= 1u << t;
+            if (valid[t] > 0) {
+              pending |= 1u << t;
+              prefetch_resid<E>(resid, e0);
+            }
           }
         }
         recv_grid<Raw, RDW, 1, kGrp>(c, slots, u, r, pending, qs);
