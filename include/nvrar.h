@@ -167,9 +167,10 @@ int nvrar_alloc_symmetric(nvrar_comm_t comm, size_t bytes, void** dev_ptr);
 int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
                     nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
 
-/* All ranks that live on ONE device (virtual ranks sharing a GPU), launched
- * as one cooperative kernel so that ranks waiting on each other are
- * co-resident. comms[i] runs send[i] -> recv[i]. `active_mask` bit i clear
+/* All ranks that live on ONE device (virtual ranks sharing a GPU) in ONE
+ * launch: cooperative when the schedule makes ranks wait on each other (so
+ * they are co-resident); with every rank present the default is the DIRECT
+ * schedule (no waits). comms[i] runs send[i] -> recv[i]. `active_mask` bit i clear
  * means comms[i] does not take part in this call (a stalled rank, used by
  * the peer-only-sync fixture); pass ~0ull for all. */
 int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* send,
