@@ -51,6 +51,58 @@ def clock_offsets(comm, rank, world, iters=50):
     return offs
 
 
+REGION = {"A": 0, "B": 1, "C": 2}  # slot areas: RS / one-shot inputs, all-gather, RD steps
+
+
+def trace_csv(args, world, nodes, offs, ref, allv) -> str:
+    """The reference's trace schema `time_us,src,dst,region,offset,bytes`
+    (bench.hpp:322-334; a row per put there) at the GPU's granularity: one row
+    per (rank, CTA, destination) push batch of the last call, timed by the
+    CTA's phase stamps on rank 0's clock (µs from rank 0's median release).
+    Regions: 0 = A slots (reduce-scatter / one-shot inputs), 1 = B (all-gather),
+    2 = C (recursive-doubling steps); offset = the batch's first byte in the
+    destination's slot."""
+    gpus = world // nodes
+    n = args.bytes // 2
+    ue_elems = 8  # bf16 Lamport: 16-byte units of 8 elements
+    rows = ["time_us,src,dst,region,offset,bytes\n"]
+
+    def units(elems):
+        return -(-elems // ue_elems)
+
+    def cta_range(u_total, b):
+        return u_total * b // args.blocks, u_total * (b + 1) // args.blocks
+
+    for r in range(world):
+        node, local = divmod(r, gpus)
+        for b, stamps in enumerate(allv[r]):
+            t_push = (stamps[3] - offs[r] - ref) / 1e3   # "pushed"
+            t_red = (stamps[5] - offs[r] - ref) / 1e3    # "reduced" (RD + all-gather pushes done)
+            batches = []
+            if args.algo in ("oneshot", "twoshot", "mcast"):
+                sp = n if args.algo != "twoshot" else -(-n // world)
+                u0, u1 = cta_range(units(sp), b)
+                for q in range(world):
+                    if q != r:
+                        batches.append((t_push, q, "A", u0, u1))
+                        if args.algo == "twoshot":
+                            batches.append((t_red, q, "B", u0, u1))
+            else:  # hier
+                u0, u1 = cta_range(units(-(-n // gpus)), b)
+                for j in range(1, gpus):
+                    batches.append((t_push, node * gpus + (local + j) % gpus, "A", u0, u1))
+                    batches.append((t_red, node * gpus + (local + j) % gpus, "B", u0, u1))
+                step = 1
+                while step < nodes:
+                    batches.append((t_red, (node ^ step) * gpus + local, "C", u0, u1))
+                    step <<= 1
+            for t, q, reg, a, z in batches:
+                if z > a:
+                    ub = 32 if reg == "C" else 16  # RD partials travel as fp32 (2x bf16)
+                    rows.append(f"{t:.3f},{r},{q},{REGION[reg]},{a * ub},{(z - a) * ub}\n")
+    return "".join(rows)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bytes", type=int, default=128 << 10)
@@ -58,6 +110,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=32)
     ap.add_argument("--nodes", type=int, default=2)
     ap.add_argument("--calls", type=int, default=20)
+    ap.add_argument("--trace-csv", default="",
+                    help="write the reference's trace CSV (bench.hpp:322-334) for the last call")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -95,6 +149,9 @@ def main():
                                           round(max(x[k] for x in rows), 3)]
                                for k in range(len(NAMES))}
         print(json.dumps(out), flush=True)
+        if args.trace_csv:
+            with open(args.trace_csv, "w") as fh:
+                fh.write(trace_csv(args, world, nodes, offs, ref, allv))
     comm._lib.nvrar_set_profile(comm._h, 0)
     dist.barrier()
     comm.close()
