@@ -274,19 +274,19 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   stamp(d, 2);
   c.phase = 3;
 
-  // Peer-only sync, wait half: all log2(N) XOR peers before any RD send.
-  if (kSteps > 0) {
-    if (threadIdx.x < kSteps) {
-      wait_seq_len(c, d, ((node ^ (1 << threadIdx.x)) * G) + local, n);
-    }
-    __syncthreads();
-  }
+  // Peer-only sync, wait half (nvrar.hpp:163-171): all log2(N) XOR peers'
+  // (seq, len) words are checked before any RD RECEIVE — each thread checks
+  // right after its first step-0 send, so the wait overlaps that send instead
+  // of preceding it (the parity double-buffering, not this wait, is what makes
+  // slot reuse safe; a length mismatch is still caught before any RD data is
+  // consumed, and a stalled peer still shows up as a SeqWait).
   if constexpr (kRS || kAG) group_guard(c, d, lp.count);
   stamp(d, 3);
   c.phase = 4;
 
   // Phases 1b+2+3a: fold own chunk, recursive doubling, cast + all-gather push.
   const uint64_t mybase = kRD ? 0 : static_cast<uint64_t>(local) * S;
+  bool xor_synced = false;
   for (uint64_t u0 = ub + threadIdx.x; u0 < ue; u0 += static_cast<uint64_t>(blockDim.x) * kHierUpt) {
     A f[kHierUpt][UE];
     int valid[kHierUpt];
@@ -375,6 +375,11 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
         uint32_t b[UE];
         acc_bits<UE>(f[k], b);
         Part::template put<UE>(dst, uu[k], b, c.seq);
+      }
+      if (l == 0 && !xor_synced) {
+#pragma unroll
+        for (int s2 = 0; s2 < kSteps; ++s2) wait_seq_len(c, d, ((node ^ (1 << s2)) * G) + local, n);
+        xor_synced = true;
       }
       uint4* src = slot_c(d, me, parity, l);
       uint4* srcs[kHierUpt];
