@@ -177,6 +177,21 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
                           void* const* recv, size_t count, nvrar_dtype_t dtype, nvrar_op_t op,
                           void* stream, uint64_t active_mask);
 
+/* Host buffers — the reference's own API shape (NvrarAllreduce<T>::run over
+ * host spans, nvrar.hpp:84-129): host_send / host_recv are HOST memory (pinned
+ * for full overlap; pageable works but copies synchronously). The vector moves
+ * through device staging in chunks (NVRAR_HOST_CHUNK bytes, default 256 KB;
+ * every rank must use the same value): the H2D copy of chunk i+1, the
+ * all-reduce of chunk i and the D2H copy of chunk i-1 overlap. Each chunk is
+ * reduced as a window of the whole vector, so the bits equal nvrar_allreduce
+ * of all `count` elements. Stream-ordered: host_recv is complete once `stream`
+ * reaches this point. */
+int nvrar_allreduce_host(nvrar_comm_t comm, const void* host_send, void* host_recv, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
+int nvrar_allreduce_local_host(nvrar_comm_t* comms, int ncomms, const void* const* host_send,
+                               void* const* host_recv, size_t count, nvrar_dtype_t dtype,
+                               nvrar_op_t op, void* stream);
+
 /* Fused epilogue for the TP-decode caller (x = x + all_reduce(a), SURVEY §8f
  * row 2): recv[i] = residual[i] + sum_r send_r[i], where the sum is the
  * all-reduce's own result (same bits as nvrar_allreduce) and the add is the

@@ -97,6 +97,10 @@ SIGNATURES = {
     "nvrar_set_plan_table": (_c.c_int, [_vp, _c.POINTER(PlanEntry), _c.c_int]),
     "nvrar_plan": (_c.c_int, [_vp, _c.c_size_t, _c.c_int, _c.POINTER(_c.c_int),
                               _c.POINTER(_c.c_int)]),
+    "nvrar_allreduce_host": (_c.c_int, [_vp, _vp, _vp, _c.c_size_t, _c.c_int, _c.c_int, _vp]),
+    "nvrar_allreduce_local_host": (_c.c_int, [_c.POINTER(_vp), _c.c_int, _c.POINTER(_vp),
+                                              _c.POINTER(_vp), _c.c_size_t, _c.c_int, _c.c_int,
+                                              _vp]),
     "nvrar_allreduce_residual": (_c.c_int, [_vp, _vp, _vp, _vp, _c.c_size_t, _c.c_int, _c.c_int,
                                             _vp]),
     "nvrar_allreduce_local_residual": (_c.c_int, [_c.POINTER(_vp), _c.c_int, _c.POINTER(_vp),

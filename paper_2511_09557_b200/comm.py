@@ -354,6 +354,15 @@ class Communicator:
         if rc:
             _raise(rc, self.last_error(), self.rank)
 
+    def allreduce_host(self, send: torch.Tensor, recv: torch.Tensor,
+                       stream: Optional[torch.cuda.Stream] = None) -> None:
+        """nvrar_allreduce_host: CPU tensors in and out (pin them for overlap);
+        stream-ordered — synchronise `stream` before reading `recv`."""
+        _check_host_pair(send, recv)
+        self._check(self._lib.nvrar_allreduce_host(self._h, send.data_ptr(), recv.data_ptr(),
+                                                   send.numel(), dtype_code(send.dtype), L.SUM,
+                                                   _stream_ptr(stream)))
+
     def allreduce_residual(self, send: torch.Tensor, residual: torch.Tensor,
                            out: Optional[torch.Tensor] = None,
                            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -439,6 +448,15 @@ def _blocked_rank(b: L.Blocked) -> BlockedRank:
                        kind=BlockedRank.Kind.SeqWait if b.kind == 1 else BlockedRank.Kind.FlagWait,
                        word_index=b.word_index, peer_rank=b.peer_rank, expected=b.expected,
                        phase=b.phase, cta=b.cta)
+
+
+def _check_host_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
+    if send.numel() != recv.numel() or send.dtype != recv.dtype:
+        raise InvalidArgumentError("nvrar: input and output differ in length or dtype")
+    if send.is_cuda or recv.is_cuda:
+        raise InvalidArgumentError("nvrar: host path takes CPU tensors")
+    if not (send.is_contiguous() and recv.is_contiguous()):
+        raise InvalidArgumentError("nvrar: buffers must be contiguous")
 
 
 def _check_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
@@ -547,6 +565,22 @@ class LocalGroup:
     def set_protocol(self, proto: str) -> None:
         for c in self.comms:
             c.set_protocol(proto)
+
+    def launch_host(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
+                    stream: Optional[torch.cuda.Stream] = None) -> None:
+        """nvrar_allreduce_local_host: every virtual rank's CPU tensors in and out."""
+        p = self.topo.world_size()
+        if len(inputs) != p or len(outputs) != p:
+            raise InvalidArgumentError("one input and one output per rank")
+        for a, b in zip(inputs, outputs):
+            _check_host_pair(a, b)
+        send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
+        recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])
+        rc = self._lib.nvrar_allreduce_local_host(self._arr, p, send, recv, inputs[0].numel(),
+                                                  dtype_code(inputs[0].dtype), L.SUM,
+                                                  _stream_ptr(stream))
+        if rc:
+            _raise(rc, self.comms[0].last_error())
 
     def plan(self, count: int, dtype: torch.dtype, active: Optional[Sequence[int]] = None):
         """(schedule, CTAs per rank) a launch of this group runs for `count` elements."""

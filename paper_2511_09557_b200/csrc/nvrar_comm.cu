@@ -89,6 +89,12 @@ struct nvrar_comm {
   uint64_t* d_scratch = nullptr;
   std::vector<nvrar_plan_entry> table;  // measured selector (ascending max_bytes)
   bool mc_ready = false;  // NVLS multicast area attached (nvrar_mc_attach)
+  // host-buffer pipeline (nvrar_allreduce_host): device staging [2 in | 2 out]
+  // of `stage_chunk` bytes each, copy streams and the events that order them
+  uint8_t* stage = nullptr;
+  size_t stage_chunk = 0;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_h2d[2] = {}, ev_ar[2] = {}, ev_d2h[2] = {};
 };
 
 namespace {
@@ -472,11 +478,26 @@ int nvrar_init(const nvrar_init_args* a, nvrar_comm_t* out) {
 
 static void mc_teardown(nvrar_comm* c);
 
+static void host_pipe_teardown(nvrar_comm* c) {
+  if (c->stage) cudaFree(c->stage);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  cudaEvent_t* evs[] = {&c->ev_start, &c->ev_h2d[0], &c->ev_h2d[1], &c->ev_ar[0], &c->ev_ar[1],
+                        &c->ev_d2h[0], &c->ev_d2h[1]};
+  for (cudaEvent_t* e : evs) {
+    if (*e) cudaEventDestroy(*e);
+    *e = nullptr;
+  }
+  c->stage = nullptr;
+  c->s_h2d = c->s_d2h = nullptr;
+}
+
 int nvrar_finalize(nvrar_comm_t c) {
   if (!c) return NVRAR_SUCCESS;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   mc_teardown(c);
+  host_pipe_teardown(c);
   for (auto* p : c->opened) cudaIpcCloseMemHandle(p);
   for (auto* p : c->sym_allocs) cudaFree(p);
   if (c->region) cudaFree(c->region);
@@ -635,7 +656,8 @@ static size_t phase_bytes(const nvrar_comm* c, int phase, size_t count, int dtyp
 static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void* const* recv,
                   size_t count, int dtype, int op, void* stream, uint64_t mask, bool local_group,
                   int phase = NVRAR_PHASE_ALL, int order = NVRAR_ORDER_NVRAR,
-                  const void* const* resid = nullptr) {
+                  const void* const* resid = nullptr, uint64_t e_off = 0,
+                  uint64_t n_order = 0) {
   nvrar_comm* c0 = comms[0];
   if (op != NVRAR_SUM) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "only SUM is supported");
   if (order < NVRAR_ORDER_NVRAR || order > NVRAR_ORDER_TREE) {
@@ -692,6 +714,8 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   if (nl == 0) return NVRAR_SUCCESS;
   lp.nlocal = nl;
   lp.count = count;
+  lp.e_off = e_off;
+  lp.n_order = n_order;
   CUDA_TRY(c0, cudaSetDevice(c0->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (count == 0) {
@@ -720,6 +744,12 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
     algo = NVRAR_ALGO_ONESHOT;
   }
   lp.mc = mc ? 1 : 0;
+  if (n_order && algo == NVRAR_ALGO_HIER) {
+    // a window of a longer vector runs on the flat schedules (their order is
+    // computed per element in the whole vector's frame)
+    algo = count * dtype_bytes(dtype) <= kOneshotMaxBytes ? NVRAR_ALGO_ONESHOT : NVRAR_ALGO_TWOSHOT;
+    if (emu) blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
+  }
   if (order != NVRAR_ORDER_NVRAR && algo != NVRAR_ALGO_ONESHOT && algo != NVRAR_ALGO_TWOSHOT) {
     // the ring / tree orders exist on the flat schedules only
     algo = count * dtype_bytes(dtype) <= (c0->world <= 4 ? (1u << 20) : (256u << 10)) &&
@@ -1067,4 +1097,121 @@ int nvrar_mc_ready(nvrar_comm_t c, int* ready) {
   if (!c || !ready) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
   *ready = c->mc_ready ? 1 : 0;
   return NVRAR_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// Host buffers (the reference's own API shape: run() over host spans). The
+// vector is moved in chunks through device staging: the H2D copy of chunk i+1,
+// the all-reduce of chunk i and the D2H copy of chunk i-1 overlap on three
+// streams. Every chunk is one all-reduce launch over a WINDOW of the whole
+// vector (LaunchParams.e_off / n_order), so the bits equal one all-reduce of
+// the whole vector — chunking must not change the reduction order.
+namespace {
+
+size_t host_chunk_bytes() {
+  static const size_t v = [] {
+    const char* e = getenv("NVRAR_HOST_CHUNK");
+    const long long b = e ? atoll(e) : 0;
+    return static_cast<size_t>(b >= 4096 ? b : 256 << 10);
+  }();
+  return v;
+}
+
+int host_pipe_ready(nvrar_comm* c, size_t chunk) {
+  if (c->stage && c->stage_chunk >= chunk) return NVRAR_SUCCESS;
+  host_pipe_teardown(c);
+  CUDA_TRY(c, cudaMalloc(&c->stage, 4 * chunk));
+  c->stage_chunk = chunk;
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+  cudaEvent_t* evs[] = {&c->ev_start, &c->ev_h2d[0], &c->ev_h2d[1], &c->ev_ar[0], &c->ev_ar[1],
+                        &c->ev_d2h[0], &c->ev_d2h[1]};
+  for (cudaEvent_t* e : evs) CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  return NVRAR_SUCCESS;
+}
+
+}  // namespace
+
+static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
+                          void* const* hrecv, size_t count, int dtype, int op, void* stream,
+                          bool local_group) {
+  nvrar_comm* c0 = comms[0];
+  if (dtype < NVRAR_INT32 || dtype > NVRAR_BF16) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  }
+  for (int i = 0; i < nc; ++i) {
+    if (!comms[i]) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "null comm %d", i);
+    if (count > 0 && (!hsend[i] || !hrecv[i])) {
+      return fail(comms[i], NVRAR_ERR_INVALID_ARGUMENT, "null buffer");
+    }
+  }
+  const size_t eb = dtype_bytes(dtype);
+  // units of 16 bytes, so every window starts on a unit boundary
+  const size_t chunk_elems = std::max<size_t>(16 / eb, host_chunk_bytes() / 16 * 16 / eb);
+  const bool windows = c0->world <= 16 && c0->gpus <= flat_max_gpus(c0->nodes);
+  const size_t ce = windows ? chunk_elems : std::max<size_t>(count, 1);
+  const size_t chunk = std::max<size_t>(ce * eb, 16);
+  for (int i = 0; i < nc; ++i) {
+    if (int rc = host_pipe_ready(comms[i], chunk)) return rc;
+  }
+  CUDA_TRY(c0, cudaSetDevice(c0->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the copies start after the work already queued on the caller's stream
+  CUDA_TRY(c0, cudaEventRecord(c0->ev_start, s));
+  CUDA_TRY(c0, cudaStreamWaitEvent(c0->s_h2d, c0->ev_start, 0));
+  if (count == 0) {
+    return launch(comms, nc, hsend, const_cast<void* const*>(hrecv), 0, dtype, op, stream,
+                  ~0ull, local_group);
+  }
+  const size_t nch = (count + ce - 1) / ce;
+  std::vector<const void*> dsend(nc);
+  std::vector<void*> drecv(nc);
+  for (size_t i = 0; i < nch; ++i) {
+    const int b = static_cast<int>(i & 1);
+    const size_t off = i * ce, cnt = std::min(ce, count - off);
+    if (i >= 2) CUDA_TRY(c0, cudaStreamWaitEvent(c0->s_h2d, c0->ev_ar[b], 0));
+    for (int r = 0; r < nc; ++r) {
+      nvrar_comm* c = comms[r];
+      uint8_t* din = c->stage + b * chunk;
+      CUDA_TRY(c0, cudaMemcpyAsync(din, static_cast<const uint8_t*>(hsend[r]) + off * eb,
+                                   cnt * eb, cudaMemcpyHostToDevice, c0->s_h2d));
+      dsend[r] = din;
+      drecv[r] = c->stage + (2 + b) * chunk;
+    }
+    CUDA_TRY(c0, cudaEventRecord(c0->ev_h2d[b], c0->s_h2d));
+    CUDA_TRY(c0, cudaStreamWaitEvent(s, c0->ev_h2d[b], 0));
+    if (i >= 2) CUDA_TRY(c0, cudaStreamWaitEvent(s, c0->ev_d2h[b], 0));
+    int rc = launch(comms, nc, dsend.data(), drecv.data(), cnt, dtype, op, stream, ~0ull,
+                    local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr,
+                    windows ? off : 0, windows ? count : 0);
+    if (rc) return rc;
+    CUDA_TRY(c0, cudaEventRecord(c0->ev_ar[b], s));
+    CUDA_TRY(c0, cudaStreamWaitEvent(c0->s_d2h, c0->ev_ar[b], 0));
+    for (int r = 0; r < nc; ++r) {
+      CUDA_TRY(c0, cudaMemcpyAsync(static_cast<uint8_t*>(hrecv[r]) + off * eb, drecv[r],
+                                   cnt * eb, cudaMemcpyDeviceToHost, c0->s_d2h));
+    }
+    CUDA_TRY(c0, cudaEventRecord(c0->ev_d2h[b], c0->s_d2h));
+  }
+  // the caller's stream completes when the last copies out have landed
+  CUDA_TRY(c0, cudaStreamWaitEvent(s, c0->ev_d2h[(nch - 1) & 1], 0));
+  if (nch > 1) CUDA_TRY(c0, cudaStreamWaitEvent(s, c0->ev_d2h[nch & 1], 0));
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_allreduce_host(nvrar_comm_t comm, const void* host_send, void* host_recv, size_t count,
+                         nvrar_dtype_t dtype, nvrar_op_t op, void* stream) {
+  if (!comm) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  const void* s[1] = {host_send};
+  void* r[1] = {host_recv};
+  return host_allreduce(&comm, 1, s, r, count, dtype, op, stream, false);
+}
+
+int nvrar_allreduce_local_host(nvrar_comm_t* comms, int ncomms, const void* const* host_send,
+                               void* const* host_recv, size_t count, nvrar_dtype_t dtype,
+                               nvrar_op_t op, void* stream) {
+  if (!comms || ncomms < 1 || ncomms > NVRAR_MAX_LOCAL || !host_send || !host_recv) {
+    return fail(comms ? comms[0] : nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad local group");
+  }
+  return host_allreduce(comms, ncomms, host_send, host_recv, count, dtype, op, stream, true);
 }

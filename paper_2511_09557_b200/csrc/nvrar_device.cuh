@@ -116,6 +116,13 @@ struct LaunchParams {
   // RNE) — bit-identical to the all-reduce followed by `resid + out`
   const void* resid[kMaxLocal];
   int mc;  // flat one-shot: push each unit once through the multicast mapping
+  // Window of a longer vector (the pipelined host-buffer path): this launch
+  // reduces elements [e_off, e_off + count) of a vector of n_order elements, so
+  // the reduction ORDER (shard index c = e / ceil(n/G)) follows the whole
+  // vector and the bits equal one all-reduce of all n_order elements.
+  // n_order = 0: the launch is the whole vector. Flat and direct kernels only.
+  uint64_t e_off;
+  uint64_t n_order;
 };
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):

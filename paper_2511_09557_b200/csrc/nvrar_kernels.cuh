@@ -522,7 +522,9 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const int order = lp.order;
   // members of one fold: the node's G ranks, or (ring order) all P ranks
   const int OG = order == kOrderRing ? P : G;
-  const uint64_t SG = (n + OG - 1) / OG;
+  const uint64_t n_ord = lp.n_order ? lp.n_order : n;  // order follows the whole vector
+  const uint64_t SG = (n_ord + OG - 1) / OG;
+  const uint32_t e_off = static_cast<uint32_t>(lp.e_off);
   constexpr uint64_t kAlign = UE;
   const uint64_t SP = oneshot ? ((n + kAlign - 1) / kAlign) * kAlign
                               : ((((n + P - 1) / P) + kAlign - 1) / kAlign) * kAlign;
@@ -646,10 +648,11 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     if (valid == 0) continue;
     prefetch_resid<E>(resid, e0);
     const bool tree = order == kOrderTree;
+    const uint32_t eg0 = e0 + e_off;  // index in the whole vector (the order's frame)
     // the tree chain does not depend on the chunk: one fixed order
-    const int c0 = tree ? 0 : static_cast<int>(e0 / SG32);
+    const int c0 = tree ? 0 : static_cast<int>(eg0 / SG32);
     const bool straddle =
-        !tree && e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32;
+        !tree && eg0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32;
     int l0 = tree ? OG - 1 : c0 + 1;
     if (l0 >= OG) l0 -= OG;
 
@@ -706,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         // The unit straddles a shard boundary: per-element fold order.
 #pragma unroll
         for (int q = 0; q < UE; ++q) {
-          const int cq = q < valid ? static_cast<int>((e0 + q) / SG32) : c0;
+          const int cq = q < valid ? static_cast<int>((eg0 + q) / SG32) : c0;
           const int rot = cq - c0;
           A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % OG, q);
 #pragma unroll
@@ -809,7 +812,9 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   begin_wait(d);
   const uint32_t n = static_cast<uint32_t>(lp.count);
   const int G = lp.d0.gpus, P = lp.nlocal;  // param space: no dependent load
-  const uint32_t SG = (n + G - 1) / G;
+  const uint32_t n_ord = lp.n_order ? static_cast<uint32_t>(lp.n_order) : n;
+  const uint32_t SG = (n_ord + G - 1) / G;  // order in the whole vector's frame
+  const uint32_t e_off = static_cast<uint32_t>(lp.e_off);
   const uint32_t U = (n + UE - 1) / UE;
   const uint32_t slice = (U + P - 1) / P;
   // small vectors leave the last ranks' slices empty (s0 clamps to U)
@@ -824,7 +829,7 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   auto load_unit = [&](uint32_t u) {
     const uint32_t e0 = UE * u;
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
-    int l0 = static_cast<int>(e0 / SG) + 1;
+    int l0 = static_cast<int>((e0 + e_off) / SG) + 1;
     if (l0 >= G) l0 -= G;
 #pragma unroll
     for (int nn = 0; nn < N; ++nn) {
@@ -842,9 +847,10 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   if (u < ue) load_unit(u);
   while (u < ue) {
     const uint32_t e0 = UE * u;
+    const uint32_t eg0 = e0 + e_off;
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
-    const int c0 = static_cast<int>(e0 / SG);
-    const bool straddle = e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG;
+    const int c0 = static_cast<int>(eg0 / SG);
+    const bool straddle = eg0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG;
     A stack[kLevels][UE];
 #pragma unroll
     for (int nn = 0; nn < N; ++nn) {
@@ -863,7 +869,7 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
       } else {
 #pragma unroll
         for (int q = 0; q < UE; ++q) {
-          const int cq = q < valid ? static_cast<int>((e0 + q) / SG) : c0;
+          const int cq = q < valid ? static_cast<int>((eg0 + q) / SG) : c0;
           const int rot = cq - c0;
           A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % G, q);
 #pragma unroll

@@ -154,6 +154,26 @@ def main():
             fails += 1
             print(f"rank {rank}: {dtype} rd_inter differs", flush=True)
 
+    # host buffers, pipelined in windows of the whole vector (bits = one call)
+    for dtype in ("f32", "bf16"):
+        n = 3 * 65536 + 1001
+        x = inputs(dtype, world, n, 980)
+        if dtype == "bf16":
+            hin = torch.from_numpy(x[rank]).view(torch.int16).view(torch.bfloat16).pin_memory()
+        else:
+            hin = torch.from_numpy(np.ascontiguousarray(x[rank])).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        comm.allreduce_host(hin, hout)
+        torch.cuda.synchronize()
+        comm.check()
+        want = O.nvrar_order_sum(x, args.nodes, args.gpus, dtype)
+        got = hout.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" else hout.numpy()
+        if dtype == "f32":
+            got, want = got.view(np.uint32), want.view(np.uint32)
+        if not np.array_equal(got, want):
+            fails += 1
+            print(f"rank {rank}: host pipeline {dtype} differs", flush=True)
+
     # fused residual epilogue: out = residual + all_reduce(x), in place
     for dtype in ("f32", "bf16"):
         n = 65539

@@ -383,3 +383,33 @@ def test_allreduce_residual_fused(nodes, gpus, algo, dtype, inplace):
                 assert np.array_equal(got.view(exp.dtype), exp), f"rank {r}"
     finally:
         g.set_algo("auto")
+
+
+@pytest.mark.parametrize("nodes,gpus", [(1, 2), (2, 2), (2, 4), (2, 3), (1, 3), (8, 1)])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+def test_host_buffer_pipeline_matches_whole_vector(nodes, gpus, dtype):
+    """nvrar_allreduce_local_host: host buffers in chunks (256 KB windows of the
+    whole vector) give the bits of ONE all-reduce of the whole vector — the
+    windows keep the whole vector's reduction order (G = 3 makes the fold order
+    depend on the element's shard, so a plain per-chunk all-reduce would differ)."""
+    g = group(nodes, gpus, max_bytes=8 << 20)
+    p = nodes * gpus
+    for n in (5, 65536 + 3, 3 * 65536 + 1001):
+        x = inputs_for(dtype, p, n, 71 + n)
+        if dtype == "bf16":
+            ins = [torch.from_numpy(x[r]).view(torch.int16).view(torch.bfloat16).pin_memory()
+                   for r in range(p)]
+        else:
+            ins = [torch.from_numpy(np.ascontiguousarray(x[r])).pin_memory() for r in range(p)]
+        outs = [torch.empty_like(t).pin_memory() for t in ins]
+        g.launch_host(ins, outs)
+        torch.cuda.synchronize()
+        g.check()
+        want = O.nvrar_order_sum(x, nodes, gpus, dtype)
+        for r in range(p):
+            got = outs[r].view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" \
+                else outs[r].numpy()
+            if dtype == "f32":
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"rank {r}"
+            else:
+                assert np.array_equal(got, want), f"rank {r}"
