@@ -180,8 +180,9 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
 /* Host buffers — the reference's own API shape (NvrarAllreduce<T>::run over
  * host spans, nvrar.hpp:84-129): host_send / host_recv are HOST memory (pinned
  * for full overlap; pageable works but copies synchronously). The vector moves
- * through device staging in chunks (NVRAR_HOST_CHUNK bytes, default 256 KB;
- * every rank must use the same value): the H2D copy of chunk i+1, the
+ * through device staging in chunks (NVRAR_HOST_CHUNK bytes if set — every rank
+ * must use the same value — else max(256 KB, bytes of all local ranks / 16)):
+ * the H2D copy of chunk i+1, the
  * all-reduce of chunk i and the D2H copy of chunk i-1 overlap. Each chunk is
  * reduced as a window of the whole vector, so the bits equal nvrar_allreduce
  * of all `count` elements. Stream-ordered: host_recv is complete once `stream`
