@@ -180,15 +180,19 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
 /* Host buffers — the reference's own API shape (NvrarAllreduce<T>::run over
  * host spans, nvrar.hpp:84-129): host_send / host_recv are HOST memory (pinned
  * for full overlap; pageable works but copies synchronously). The vector moves
- * through device staging in chunks (NVRAR_HOST_CHUNK bytes if set — every rank
- * must use the same value — else max(256 KB, bytes of all local ranks / 16)):
- * the H2D copy of chunk i+1, the
+ * through device staging, in chunks when the local ranks move more than 4 MB
+ * (NVRAR_HOST_CHUNK bytes per rank overrides; every rank must use the same
+ * value): the H2D copy of chunk i+1, the
  * all-reduce of chunk i and the D2H copy of chunk i-1 overlap. Each chunk is
  * reduced as a window of the whole vector, so the bits equal nvrar_allreduce
  * of all `count` elements. Stream-ordered: host_recv is complete once `stream`
  * reaches this point. */
 int nvrar_allreduce_host(nvrar_comm_t comm, const void* host_send, void* host_recv, size_t count,
                          nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
+/* Chunk (bytes per rank) of the host pipeline for this comm; 0 = automatic.
+ * Every rank must set the same value (the chunking is part of the call
+ * sequence). For a local group, comms[0]'s value applies. */
+int nvrar_set_host_chunk(nvrar_comm_t comm, size_t bytes);
 int nvrar_allreduce_local_host(nvrar_comm_t* comms, int ncomms, const void* const* host_send,
                                void* const* host_recv, size_t count, nvrar_dtype_t dtype,
                                nvrar_op_t op, void* stream);

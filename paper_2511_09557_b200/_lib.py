@@ -98,6 +98,7 @@ SIGNATURES = {
     "nvrar_plan": (_c.c_int, [_vp, _c.c_size_t, _c.c_int, _c.POINTER(_c.c_int),
                               _c.POINTER(_c.c_int)]),
     "nvrar_allreduce_host": (_c.c_int, [_vp, _vp, _vp, _c.c_size_t, _c.c_int, _c.c_int, _vp]),
+    "nvrar_set_host_chunk": (_c.c_int, [_vp, _c.c_size_t]),
     "nvrar_allreduce_local_host": (_c.c_int, [_c.POINTER(_vp), _c.c_int, _c.POINTER(_vp),
                                               _c.POINTER(_vp), _c.c_size_t, _c.c_int, _c.c_int,
                                               _vp]),

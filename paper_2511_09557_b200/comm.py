@@ -354,6 +354,10 @@ class Communicator:
         if rc:
             _raise(rc, self.last_error(), self.rank)
 
+    def set_host_chunk(self, nbytes: int) -> None:
+        """Chunk of the host-buffer pipeline (0 = automatic); same on every rank."""
+        self._check(self._lib.nvrar_set_host_chunk(self._h, nbytes))
+
     def allreduce_host(self, send: torch.Tensor, recv: torch.Tensor,
                        stream: Optional[torch.cuda.Stream] = None) -> None:
         """nvrar_allreduce_host: CPU tensors in and out (pin them for overlap);
@@ -565,6 +569,10 @@ class LocalGroup:
     def set_protocol(self, proto: str) -> None:
         for c in self.comms:
             c.set_protocol(proto)
+
+    def set_host_chunk(self, nbytes: int) -> None:
+        for c in self.comms:
+            c.set_host_chunk(nbytes)
 
     def launch_host(self, inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
                     stream: Optional[torch.cuda.Stream] = None) -> None:

@@ -93,6 +93,7 @@ struct nvrar_comm {
   // of `stage_chunk` bytes each, copy streams and the events that order them
   uint8_t* stage = nullptr;
   size_t stage_chunk = 0;
+  size_t host_chunk = 0;  // nvrar_set_host_chunk (0 = automatic)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_start = nullptr, ev_h2d[2] = {}, ev_ar[2] = {}, ev_d2h[2] = {};
 };
@@ -1108,17 +1109,20 @@ int nvrar_mc_ready(nvrar_comm_t c, int* ready) {
 // the whole vector — chunking must not change the reduction order.
 namespace {
 
-// Chunk of the host pipeline: NVRAR_HOST_CHUNK if set, else 256 KB, grown
-// with the bytes all local ranks move so the per-copy launch cost stays small
-// (measured: 1 MB at P=4 -> 256 KB chunks; 8 virtual ranks x 1 MB -> 512 KB).
-// A function of (count, dtype, local ranks) only, so every rank agrees.
-size_t host_chunk_bytes(size_t total_bytes) {
+// Chunk of the host pipeline (bytes per rank): NVRAR_HOST_CHUNK if set; else
+// the whole vector while all local ranks move <= 4 MB (measured: the copies'
+// per-launch and cross-stream costs eat the overlap at 1 MB per rank — P=2
+// 65 us unchunked vs 87 us in 256 KB chunks), above that max(512 KB, 1/4 of
+// the vector). A function of (count, dtype, local ranks) only: ranks agree.
+size_t host_chunk_bytes(const nvrar_comm* c, size_t rank_bytes, int nc) {
   static const long long env = [] {
     const char* e = getenv("NVRAR_HOST_CHUNK");
     return e ? atoll(e) : 0LL;
   }();
+  if (c->host_chunk) return c->host_chunk;
   if (env >= 4096) return static_cast<size_t>(env);
-  return std::max<size_t>(256 << 10, total_bytes / 16);
+  if (rank_bytes * static_cast<size_t>(nc) <= (4u << 20)) return std::max<size_t>(rank_bytes, 16);
+  return std::max<size_t>(512 << 10, rank_bytes / 4);
 }
 
 int host_pipe_ready(nvrar_comm* c, size_t chunk) {
@@ -1152,7 +1156,7 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
   const size_t eb = dtype_bytes(dtype);
   // units of 16 bytes, so every window starts on a unit boundary
   const size_t chunk_elems =
-      std::max<size_t>(16 / eb, host_chunk_bytes(count * eb * nc) / 16 * 16 / eb);
+      std::max<size_t>(16 / eb, (host_chunk_bytes(c0, count * eb, nc) + 15) / 16 * 16 / eb);
   const bool windows = c0->world <= 16 && c0->gpus <= flat_max_gpus(c0->nodes);
   const size_t ce = windows ? chunk_elems : std::max<size_t>(count, 1);
   const size_t chunk = std::max<size_t>(ce * eb, 16);
@@ -1161,9 +1165,6 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
   }
   CUDA_TRY(c0, cudaSetDevice(c0->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // the copies start after the work already queued on the caller's stream
-  CUDA_TRY(c0, cudaEventRecord(c0->ev_start, s));
-  CUDA_TRY(c0, cudaStreamWaitEvent(c0->s_h2d, c0->ev_start, 0));
   if (count == 0) {
     return launch(comms, nc, hsend, const_cast<void* const*>(hrecv), 0, dtype, op, stream,
                   ~0ull, local_group);
@@ -1171,6 +1172,26 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
   const size_t nch = (count + ce - 1) / ce;
   std::vector<const void*> dsend(nc);
   std::vector<void*> drecv(nc);
+  if (nch == 1) {
+    // one chunk: everything on the caller's stream (no cross-stream hops)
+    for (int r = 0; r < nc; ++r) {
+      dsend[r] = comms[r]->stage;
+      drecv[r] = comms[r]->stage + 2 * chunk;
+      CUDA_TRY(c0, cudaMemcpyAsync(comms[r]->stage, hsend[r], count * eb,
+                                   cudaMemcpyHostToDevice, s));
+    }
+    if (int rc = launch(comms, nc, dsend.data(), drecv.data(), count, dtype, op, stream, ~0ull,
+                        local_group)) {
+      return rc;
+    }
+    for (int r = 0; r < nc; ++r) {
+      CUDA_TRY(c0, cudaMemcpyAsync(hrecv[r], drecv[r], count * eb, cudaMemcpyDeviceToHost, s));
+    }
+    return NVRAR_SUCCESS;
+  }
+  // the copies start after the work already queued on the caller's stream
+  CUDA_TRY(c0, cudaEventRecord(c0->ev_start, s));
+  CUDA_TRY(c0, cudaStreamWaitEvent(c0->s_h2d, c0->ev_start, 0));
   for (size_t i = 0; i < nch; ++i) {
     const int b = static_cast<int>(i & 1);
     const size_t off = i * ce, cnt = std::min(ce, count - off);
@@ -1219,4 +1240,11 @@ int nvrar_allreduce_local_host(nvrar_comm_t* comms, int ncomms, const void* cons
     return fail(comms ? comms[0] : nullptr, NVRAR_ERR_INVALID_ARGUMENT, "bad local group");
   }
   return host_allreduce(comms, ncomms, host_send, host_recv, count, dtype, op, stream, true);
+}
+
+int nvrar_set_host_chunk(nvrar_comm_t c, size_t bytes) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  if (bytes != 0 && bytes < 16) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "chunk < 16 bytes");
+  c->host_chunk = bytes;
+  return NVRAR_SUCCESS;
 }

@@ -163,7 +163,9 @@ def main():
         else:
             hin = torch.from_numpy(np.ascontiguousarray(x[rank])).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
+        comm.set_host_chunk(256 << 10)  # several windows per vector
         comm.allreduce_host(hin, hout)
+        comm.set_host_chunk(0)
         torch.cuda.synchronize()
         comm.check()
         want = O.nvrar_order_sum(x, args.nodes, args.gpus, dtype)

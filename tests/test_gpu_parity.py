@@ -394,6 +394,7 @@ def test_host_buffer_pipeline_matches_whole_vector(nodes, gpus, dtype):
     depend on the element's shard, so a plain per-chunk all-reduce would differ)."""
     g = group(nodes, gpus, max_bytes=8 << 20)
     p = nodes * gpus
+    g.set_host_chunk(256 << 10)  # several windows per vector
     for n in (5, 65536 + 3, 3 * 65536 + 1001):
         x = inputs_for(dtype, p, n, 71 + n)
         if dtype == "bf16":
@@ -413,3 +414,4 @@ def test_host_buffer_pipeline_matches_whole_vector(nodes, gpus, dtype):
                 assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"rank {r}"
             else:
                 assert np.array_equal(got, want), f"rank {r}"
+    g.set_host_chunk(0)
