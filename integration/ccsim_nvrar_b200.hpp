@@ -78,6 +78,26 @@ class NvrarB200Allreduce {
     throw_on(nvrar_check(comm_), comm_);  // synchronises; device faults -> exceptions
   }
 
+  /// The reference's exact call shape: HOST spans in and out (nvrar.hpp:84-129).
+  /// The vector is staged through device memory (chunk-pipelined for large
+  /// vectors); the bits equal run() on device buffers. Pinned host memory
+  /// (cudaHostRegister / cudaMallocHost) gives full copy/compute overlap.
+  void run_host(std::span<const T> in, std::span<T> out, const NvrarConfig& cfg = {},
+                void* stream = nullptr) {
+    cfg.validate();
+    if (in.size() != out.size()) {
+      throw InvalidArgumentError("nvrar: input and output lengths differ");
+    }
+    if (in.size() > max_elems_) {
+      throw InvalidArgumentError("nvrar: vector longer than the preallocated maximum");
+    }
+    throw_on(nvrar_set_config(comm_, cfg.blocks, cfg.chunk_bytes), comm_);
+    throw_on(nvrar_allreduce_host(comm_, in.data(), out.data(), in.size(), dtype(), NVRAR_SUM,
+                                  stream),
+             comm_);
+    throw_on(nvrar_check(comm_), comm_);  // synchronises: `out` is complete on return
+  }
+
   /// Inter-node phase only (NvrarAllreduce<T>::rd_inter, nvrar.hpp:132-155):
   /// `packed` = this rank's shard as fused words {data, seq} packed with
   /// sequence()+1; `out` receives the reduced shard packed with that call.

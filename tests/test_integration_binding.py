@@ -24,6 +24,7 @@ void uses(ccsim::NvrarB200Allreduce<T>& c) {
   std::span<const std::uint64_t> pk;
   std::span<std::uint64_t> po;
   c.run(in, out, ccsim::NvrarConfig{}, nullptr);
+  c.run_host(in, out, ccsim::NvrarConfig{}, nullptr);
   c.rd_inter(pk, po, ccsim::NvrarConfig{}, nullptr);
   c.reduce_scatter(in, out, nullptr);
   c.all_gather(in, out, nullptr);
