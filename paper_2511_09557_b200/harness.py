@@ -115,14 +115,17 @@ class ClockSampler:
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                if self._nvml is not None:
-                    self._sample_nvml()
-                else:
-                    self._sample_smi()
-            except Exception:
-                pass
+            self._sample()
             self._stop.wait(0.001 if self._nvml is not None else 0.2)
+
+    def _sample(self):
+        try:
+            if self._nvml is not None:
+                self._sample_nvml()
+            else:
+                self._sample_smi()
+        except Exception:
+            pass
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -130,6 +133,10 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        # a last sample at the end of the region (a short region may otherwise
+        # see only the thread's first sample)
+        if self._nvml is not None:
+            self._sample()
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
