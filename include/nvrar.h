@@ -178,9 +178,11 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
                           void* stream, uint64_t active_mask);
 
 /* Host buffers — the reference's own API shape (NvrarAllreduce<T>::run over
- * host spans, nvrar.hpp:84-129): host_send / host_recv are HOST memory (pinned
- * for full overlap; pageable works but copies synchronously). The vector moves
- * through device staging, in chunks when the local ranks move more than 4 MB
+ * host spans, nvrar.hpp:84-129): host_send / host_recv are HOST memory. Pinned
+ * (device-mapped) buffers are used in place: the kernels read the inputs and
+ * write the results over PCIe themselves (zero-copy; the transfers overlap the
+ * exchange). Otherwise — or with an explicit nvrar_set_host_chunk — the vector
+ * moves through device staging, in chunks when the local ranks move more than 4 MB
  * (NVRAR_HOST_CHUNK bytes per rank overrides; every rank must use the same
  * value): the H2D copy of chunk i+1, the
  * all-reduce of chunk i and the D2H copy of chunk i-1 overlap. Each chunk is

@@ -1154,6 +1154,30 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
     }
   }
   const size_t eb = dtype_bytes(dtype);
+  CUDA_TRY(c0, cudaSetDevice(c0->device));
+  // Zero-copy: pinned host memory is mapped into the device's address space
+  // (UVA), so the kernels read the inputs and write the results over PCIe
+  // themselves — no staging copies, the transfers overlap the exchange.
+  bool mapped = count > 0;
+  std::vector<const void*> zsend(nc);
+  std::vector<void*> zrecv(nc);
+  for (int r = 0; r < nc && mapped; ++r) {
+    cudaPointerAttributes a{}, b{};
+    if (cudaPointerGetAttributes(&a, hsend[r]) != cudaSuccess ||
+        cudaPointerGetAttributes(&b, hrecv[r]) != cudaSuccess ||
+        a.type != cudaMemoryTypeHost || b.type != cudaMemoryTypeHost || !a.devicePointer ||
+        !b.devicePointer) {
+      mapped = false;
+      cudaGetLastError();
+      break;
+    }
+    zsend[r] = a.devicePointer;
+    zrecv[r] = b.devicePointer;
+  }
+  if (mapped && !c0->host_chunk) {
+    return launch(comms, nc, zsend.data(), zrecv.data(), count, dtype, op, stream, ~0ull,
+                  local_group);
+  }
   // units of 16 bytes, so every window starts on a unit boundary
   const size_t chunk_elems =
       std::max<size_t>(16 / eb, (host_chunk_bytes(c0, count * eb, nc) + 15) / 16 * 16 / eb);

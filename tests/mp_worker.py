@@ -166,6 +166,14 @@ def main():
         comm.set_host_chunk(256 << 10)  # several windows per vector
         comm.allreduce_host(hin, hout)
         comm.set_host_chunk(0)
+        hout2 = torch.empty_like(hin).pin_memory()
+        comm.allreduce_host(hin, hout2)  # zero-copy: the kernels use the pinned buffers
+        torch.cuda.synchronize()
+        comm.check()
+        if not torch.equal(hout.view(torch.int16) if dtype == "bf16" else hout,
+                           hout2.view(torch.int16) if dtype == "bf16" else hout2):
+            fails += 1
+            print(f"rank {rank}: zero-copy host path {dtype} differs", flush=True)
         torch.cuda.synchronize()
         comm.check()
         want = O.nvrar_order_sum(x, args.nodes, args.gpus, dtype)

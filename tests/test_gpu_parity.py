@@ -387,14 +387,18 @@ def test_allreduce_residual_fused(nodes, gpus, algo, dtype, inplace):
 
 @pytest.mark.parametrize("nodes,gpus", [(1, 2), (2, 2), (2, 4), (2, 3), (1, 3), (8, 1)])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
-def test_host_buffer_pipeline_matches_whole_vector(nodes, gpus, dtype):
-    """nvrar_allreduce_local_host: host buffers in chunks (256 KB windows of the
-    whole vector) give the bits of ONE all-reduce of the whole vector — the
-    windows keep the whole vector's reduction order (G = 3 makes the fold order
-    depend on the element's shard, so a plain per-chunk all-reduce would differ)."""
+@pytest.mark.parametrize("chunk", [0, 256 << 10])
+def test_host_buffer_pipeline_matches_whole_vector(nodes, gpus, dtype, chunk):
+    """nvrar_allreduce_local_host: pinned host buffers used in place (zero-copy)
+    or staged in chunks (256 KB windows of the whole vector) give the bits of ONE
+    all-reduce of the whole vector — the windows keep the whole vector's
+    reduction order (G = 3 makes the fold order depend on the element's shard,
+    so a plain per-chunk all-reduce would differ)."""
     g = group(nodes, gpus, max_bytes=8 << 20)
     p = nodes * gpus
-    g.set_host_chunk(256 << 10)  # several windows per vector
+    # 0: pinned buffers are read / written in place by the kernels (zero-copy);
+    # 256 KB: staged in several windows per vector
+    g.set_host_chunk(chunk)
     for n in (5, 65536 + 3, 3 * 65536 + 1001):
         x = inputs_for(dtype, p, n, 71 + n)
         if dtype == "bf16":
