@@ -250,7 +250,7 @@ def run_emulated(args):
                          "kind": cpu_kind, "sample": cpu_sample},
         "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
                 "h2d_bytes_per_step": P * msg, "d2h_bytes_per_step": P * msg,
-                "path": "nvrar_allreduce_local_host (pinned host buffers, chunk-pipelined)"},
+                "path": "nvrar_allreduce_local_host (pinned host buffers, zero-copy)"},
         "gpu_launches": (args.steps + args.warmup) * calls,
         "clocks": clk.summary(),
         "sweep": sweep,
@@ -402,7 +402,7 @@ def run_multi(args, rank, world, local):
             "cpu_baseline": None,
             "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
                     "h2d_bytes_per_step": msg, "d2h_bytes_per_step": msg,
-                    "path": "nvrar_allreduce_host (pinned host buffers, chunk-pipelined)"},
+                    "path": "nvrar_allreduce_host (pinned host buffers, zero-copy)"},
             "gpu_launches": (args.steps + args.warmup) * calls,
             "clocks": clk.summary(),
             "sweep": sweep,

@@ -79,9 +79,9 @@ class NvrarB200Allreduce {
   }
 
   /// The reference's exact call shape: HOST spans in and out (nvrar.hpp:84-129).
-  /// The vector is staged through device memory (chunk-pipelined for large
-  /// vectors); the bits equal run() on device buffers. Pinned host memory
-  /// (cudaHostRegister / cudaMallocHost) gives full copy/compute overlap.
+  /// Pinned host memory (cudaHostRegister / cudaMallocHost) is used in place by
+  /// the kernels (zero-copy over PCIe); pageable memory is staged through device
+  /// memory. Either way the bits equal run() on device buffers.
   void run_host(std::span<const T> in, std::span<T> out, const NvrarConfig& cfg = {},
                 void* stream = nullptr) {
     cfg.validate();
