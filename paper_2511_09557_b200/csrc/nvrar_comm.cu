@@ -570,7 +570,7 @@ int nvrar_plan(nvrar_comm_t c, size_t count, nvrar_dtype_t dtype, int* algo, int
 }
 
 static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, int* algo_out,
-                    int* blocks_out);
+                    int* blocks_out, int upt = 1);
 
 int nvrar_plan_local(nvrar_comm_t* comms, int ncomms, size_t count, nvrar_dtype_t dtype,
                      uint64_t active_mask, int* algo, int* blocks) {
@@ -623,7 +623,7 @@ int nvrar_get_peers(nvrar_comm_t c, int* peers, int max_peers, int* steps) {
 // The schedule and CTAs per rank a launch of nl ranks of c0's topology uses
 // (emu: the ranks are virtual ranks of one local group, one launch).
 static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, int* algo_out,
-                    int* blocks_out) {
+                    int* blocks_out, int upt) {
   int algo = 0, blocks = 1;
   plan(c0, count, dtype, &algo, &blocks, emu && nl > 1);
   // the direct schedule needs every rank of the topology in this launch
@@ -633,8 +633,10 @@ static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, i
     // SM while every CTA keeps >= a warp of units, at most one unit per thread,
     // and no more CTAs than fit at once (threads loop, prefetching the next unit)
     const size_t upr = ((count * dtype_bytes(dtype) + 15) / 16 + nl - 1) / nl;
-    const size_t full = (upr + kDirectThreads - 1) / kDirectThreads;
-    const size_t spread = std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
+    // upt > 1 (host buffers over PCIe): fewer CTAs, each thread loops, so the
+    // loads of unit i+1 overlap the stores of unit i across the link
+    const size_t full = (upr + kDirectThreads * upt - 1) / (kDirectThreads * upt);
+    const size_t spread = upt > 1 ? 1 : std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
     const size_t resident = std::max(1, c0->direct_ctas[dtype] / nl);
     blocks = static_cast<int>(std::max<size_t>(
         1, std::min<size_t>({std::max(full, spread), resident, static_cast<size_t>(kSeqSlots)})));
@@ -658,7 +660,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
                   size_t count, int dtype, int op, void* stream, uint64_t mask, bool local_group,
                   int phase = NVRAR_PHASE_ALL, int order = NVRAR_ORDER_NVRAR,
                   const void* const* resid = nullptr, uint64_t e_off = 0,
-                  uint64_t n_order = 0) {
+                  uint64_t n_order = 0, int upt = 1) {
   nvrar_comm* c0 = comms[0];
   if (op != NVRAR_SUM) return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "only SUM is supported");
   if (order < NVRAR_ORDER_NVRAR || order > NVRAR_ORDER_TREE) {
@@ -729,7 +731,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   const bool emu = local_group;
   resolve(c0, nl, phase == NVRAR_PHASE_ALL ? count : phase_bytes(c0, phase, count, dtype) /
                                                          dtype_bytes(dtype),
-          dtype, emu, &algo, &blocks);
+          dtype, emu, &algo, &blocks, upt);
   if (phase != NVRAR_PHASE_ALL) {
     // the phase-only entry points run the hierarchical kernel's phase code
     algo = NVRAR_ALGO_HIER;
@@ -1109,6 +1111,15 @@ int nvrar_mc_ready(nvrar_comm_t c, int* ready) {
 // the whole vector — chunking must not change the reduction order.
 namespace {
 
+// Units per thread the direct schedule's grid is sized for when its buffers are
+// host memory read and written over PCIe (env NVRAR_HOST_UPT; default 8 —
+// measured N=1 e2e: 1 unit 321 us, 4 units 261 us, 8 units 246 us, 16 261 us).
+const int kHostUnitsPerThread = [] {
+  const char* e = getenv("NVRAR_HOST_UPT");
+  const int v = e ? atoi(e) : 8;
+  return v >= 1 && v <= 64 ? v : 8;
+}();
+
 // Chunk of the host pipeline (bytes per rank): NVRAR_HOST_CHUNK if set; else
 // the whole vector while all local ranks move <= 4 MB (measured: the copies'
 // per-launch and cross-stream costs eat the overlap at 1 MB per rank — P=2
@@ -1176,7 +1187,8 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
   }
   if (mapped && !c0->host_chunk) {
     return launch(comms, nc, zsend.data(), zrecv.data(), count, dtype, op, stream, ~0ull,
-                  local_group);
+                  local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr, 0, 0,
+                  kHostUnitsPerThread);
   }
   // units of 16 bytes, so every window starts on a unit boundary
   const size_t chunk_elems =
