@@ -643,6 +643,12 @@ static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, i
   } else if (emu) {
     blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   }
+  if (upt > 1 && algo != NVRAR_ALGO_DIRECT) {
+    // host buffers over PCIe: at most 64 CTAs, so threads loop and the link
+    // reads/writes of consecutive units overlap (measured at 1 MB: P=2
+    // 63.8 -> 53.7 us, P=4 65.2 -> 57.0 us against 128 CTAs)
+    blocks = std::min(blocks, 64);
+  }
   *algo_out = algo;
   *blocks_out = blocks;
 }
