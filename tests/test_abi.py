@@ -120,3 +120,17 @@ def test_selector_default_policy_and_fallbacks():
     assert plan_for(32, 8, 4, 1000, L.BF16, algo=L.ALGO_MCAST)[0] == "hier"
     # the direct schedule exists only for a local group of virtual ranks
     assert plan_for(8, 2, 4, 1000, L.FLOAT32, algo=L.ALGO_DIRECT)[0] == "hier"
+
+
+def test_host_buffer_argument_checks():
+    """The host-buffer path's Python checks (no device needed)."""
+    import torch
+    from paper_2511_09557_b200.comm import InvalidArgumentError, _check_host_pair
+    a = torch.zeros(16, dtype=torch.float32)
+    _check_host_pair(a, torch.zeros(16, dtype=torch.float32))
+    with pytest.raises(InvalidArgumentError):
+        _check_host_pair(a, torch.zeros(8, dtype=torch.float32))
+    with pytest.raises(InvalidArgumentError):
+        _check_host_pair(a, torch.zeros(16, dtype=torch.bfloat16))
+    with pytest.raises(InvalidArgumentError):
+        _check_host_pair(torch.zeros(32)[::2], torch.zeros(16))
