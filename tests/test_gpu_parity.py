@@ -419,3 +419,17 @@ def test_host_buffer_pipeline_matches_whole_vector(nodes, gpus, dtype, chunk):
             else:
                 assert np.array_equal(got, want), f"rank {r}"
     g.set_host_chunk(0)
+
+
+def test_host_buffer_pageable_memory():
+    """Pageable (unpinned) host buffers take the staged path — same bits."""
+    g = group(2, 2)
+    x = inputs_for("f32", 4, 70001, 91)
+    ins = [torch.from_numpy(np.ascontiguousarray(x[r])) for r in range(4)]  # not pinned
+    outs = [torch.empty_like(t) for t in ins]
+    g.launch_host(ins, outs)
+    torch.cuda.synchronize()
+    g.check()
+    want = O.nvrar_order_sum(x, 2, 2).view(np.uint32)
+    for r in range(4):
+        assert np.array_equal(outs[r].numpy().view(np.uint32), want)
