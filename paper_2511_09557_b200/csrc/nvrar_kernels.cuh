@@ -30,7 +30,17 @@
 // flat_kernel — the same order on a flat schedule (B200-first: every peer is
 //   one NVSwitch hop away, so the hierarchy only has to fix the ORDER):
 //   two-shot = flat reduce-scatter (rank p owns elements [p*SP, (p+1)*SP)) +
-//   flat all-gather; one-shot = every rank receives every input.
+//   flat all-gather; one-shot = every rank receives every input (optionally
+//   pushed once through an NVSwitch multicast mapping). It also evaluates the
+//   reference's ring and tree orders (LaunchParams.order) and windows of a
+//   longer vector (LaunchParams.e_off / n_order, the host-buffer pipeline).
+//
+// direct_kernel — virtual ranks sharing one GPU, all in one launch: each unit
+//   is folded once from every rank's input and written to every output.
+//
+// Every kernel's final store can fuse the residual add (nvrar_allreduce_residual)
+// and hier_kernel<..., MODE> also runs one phase on its own (phase-only entry
+// points). Kernels are specialised on the node count and on the group size.
 //
 // Reuse safety without any barrier: every slot set is double-buffered by call
 // parity (nvrar.hpp:107-109,124-126) and re-emptied by its reader. A rank can
