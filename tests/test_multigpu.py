@@ -91,8 +91,9 @@ def test_mixed_call_stress(world):
     assert out.count(": OK after 600 calls") == world, out[-4000:]
 
 
-def test_eight_rank_layout_on_fewer_gpus():
-    """The P=8 layout (2x4, configs[1]) with 8 processes on 4 GPUs: two ranks
+@pytest.mark.parametrize("nodes,gpus", [(2, 4), (4, 2), (8, 1)])
+def test_eight_rank_layout_on_fewer_gpus(nodes, gpus):
+    """The P=8 layouts (2x4 configs[1]; 4x2, 8x1 configs[2]) with 8 processes on 4 GPUs: two ranks
     share a device and progress by time-slicing, so every non-virtual P=8 kernel
     instantiation (flat N=2 x MAXG=4, hierarchical N=2 x MG=4) and the 8-rank
     bootstrap run against the oracle (timing meaningless)."""
@@ -100,6 +101,6 @@ def test_eight_rank_layout_on_fewer_gpus():
         pytest.skip("needs 4 GPUs")
     if NDEV >= 8:
         pytest.skip("8 GPUs present: test_multiprocess_parity covers P=8 directly")
-    rc, out = _run(8, 2, 4, ("--dev-mod", "4", "--quick"))
+    rc, out = _run(8, nodes, gpus, ("--dev-mod", "4", "--quick"))
     assert rc == 0, out[-4000:]
     assert out.count(": OK") == 8, out[-4000:]
