@@ -1192,15 +1192,43 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
     zrecv[r] = b.devicePointer;
   }
   if (mapped && !c0->host_chunk) {
-    return launch(comms, nc, zsend.data(), zrecv.data(), count, dtype, op, stream, ~0ull,
-                  local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr, 0, 0,
-                  kHostUnitsPerThread);
+    if (count * eb <= c0->max_bytes) {
+      return launch(comms, nc, zsend.data(), zrecv.data(), count, dtype, op, stream, ~0ull,
+                    local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr, 0, 0,
+                    kHostUnitsPerThread);
+    }
+    // longer than the staging the comm was sized for: windows of the whole
+    // vector straight over the mapped host memory (same bits as one call)
+    if (c0->world > 16 || c0->gpus > flat_max_gpus(c0->nodes)) {
+      return fail(c0, NVRAR_ERR_INVALID_ARGUMENT,
+                  "nvrar: vector longer than the preallocated maximum (%zu B > %zu B)",
+                  count * eb, c0->max_bytes);
+    }
+    const size_t we = c0->max_bytes / eb / 16 * 16;  // window elements, unit aligned
+    std::vector<const void*> ws(nc);
+    std::vector<void*> wr(nc);
+    for (size_t off = 0; off < count; off += we) {
+      const size_t cnt = std::min(we, count - off);
+      for (int r = 0; r < nc; ++r) {
+        ws[r] = static_cast<const uint8_t*>(zsend[r]) + off * eb;
+        wr[r] = static_cast<uint8_t*>(zrecv[r]) + off * eb;
+      }
+      if (int rc = launch(comms, nc, ws.data(), wr.data(), cnt, dtype, op, stream, ~0ull,
+                          local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr, off, count,
+                          kHostUnitsPerThread)) {
+        return rc;
+      }
+    }
+    return NVRAR_SUCCESS;
   }
   // units of 16 bytes, so every window starts on a unit boundary
   const size_t chunk_elems =
       std::max<size_t>(16 / eb, (host_chunk_bytes(c0, count * eb, nc) + 15) / 16 * 16 / eb);
   const bool windows = c0->world <= 16 && c0->gpus <= flat_max_gpus(c0->nodes);
-  const size_t ce = windows ? chunk_elems : std::max<size_t>(count, 1);
+  // a window never exceeds what the comm's staging was sized for
+  const size_t ce = windows ? std::min(chunk_elems, std::max<size_t>(16 / eb,
+                                                                    c0->max_bytes / eb / 16 * 16))
+                            : std::max<size_t>(count, 1);
   const size_t chunk = std::max<size_t>(ce * eb, 16);
   for (int i = 0; i < nc; ++i) {
     if (int rc = host_pipe_ready(comms[i], chunk)) return rc;

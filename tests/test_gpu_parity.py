@@ -433,3 +433,23 @@ def test_host_buffer_pageable_memory():
     want = O.nvrar_order_sum(x, 2, 2).view(np.uint32)
     for r in range(4):
         assert np.array_equal(outs[r].numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("chunk", [0, 64 << 10])
+def test_host_buffer_longer_than_max_bytes(chunk):
+    """A host vector longer than the comm's max_bytes runs as windows of the
+    whole vector (zero-copy or staged) — still the bits of one all-reduce."""
+    g = LocalGroup(ClusterTopology(2, 3), 256 << 10, device=DEV, timeout_s=20.0)
+    try:
+        g.set_host_chunk(chunk)
+        x = inputs_for("f32", 6, 300001, 93)
+        ins = [torch.from_numpy(np.ascontiguousarray(x[r])).pin_memory() for r in range(6)]
+        outs = [torch.empty_like(t).pin_memory() for t in ins]
+        g.launch_host(ins, outs)
+        torch.cuda.synchronize()
+        g.check()
+        want = O.nvrar_order_sum(x, 2, 3).view(np.uint32)
+        for r in range(6):
+            assert np.array_equal(outs[r].numpy().view(np.uint32), want), f"rank {r}"
+    finally:
+        g.close()
