@@ -54,8 +54,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {src}")
         if verbose:
             sys.stderr.write(r.stderr)
+        # the per-function "Compile time" lines vary run to run; drop them so a
+        # rebuild leaves the tracked register/spill report unchanged
+        report = "".join(l for l in r.stderr.splitlines(keepends=True)
+                         if "Compile time" not in l)
         with open(obj + ".ptxas.txt", "w") as fh:
-            fh.write(r.stderr)
+            fh.write(report)
         return obj
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
