@@ -182,16 +182,20 @@ int nvrar_allreduce_local(nvrar_comm_t* comms, int ncomms, const void* const* se
  * (device-mapped) buffers are used in place: the kernels read the inputs and
  * write the results over PCIe themselves (zero-copy; the transfers overlap the
  * exchange). Otherwise — or with an explicit nvrar_set_host_chunk — the vector
- * moves through device staging, in chunks when the local ranks move more than 4 MB
- * (NVRAR_HOST_CHUNK bytes per rank overrides; every rank must use the same
- * value): the H2D copy of chunk i+1, the
- * all-reduce of chunk i and the D2H copy of chunk i-1 overlap. Each chunk is
- * reduced as a window of the whole vector, so the bits equal nvrar_allreduce
- * of all `count` elements. Stream-ordered: host_recv is complete once `stream`
- * reaches this point. */
+ * moves through device staging. The vector is processed in WINDOWS: one window
+ * (one launch) unless it is longer than the comm's max_bytes or a host chunk is
+ * set (nvrar_set_host_chunk, or NVRAR_HOST_CHUNK bytes per rank); with several
+ * windows the staged path overlaps the H2D copy of window i+1, the all-reduce
+ * of window i and the D2H copy of window i-1. The window schedule depends only
+ * on (count, dtype, max_bytes, host chunk) — never on whether a rank's buffers
+ * are pinned — so ranks mixing pinned and pageable memory issue the same
+ * launches. Each window is reduced as a window of the whole vector, so the bits
+ * equal nvrar_allreduce of all `count` elements. Vectors of 2^31 or more
+ * elements are rejected (INVALID_ARGUMENT). Stream-ordered: host_recv is
+ * complete once `stream` reaches this point. */
 int nvrar_allreduce_host(nvrar_comm_t comm, const void* host_send, void* host_recv, size_t count,
                          nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
-/* Chunk (bytes per rank) of the host pipeline for this comm; 0 = automatic.
+/* Window (bytes per rank) of the host path for this comm; 0 = automatic.
  * Every rank must set the same value (the chunking is part of the call
  * sequence). For a local group, comms[0]'s value applies. */
 int nvrar_set_host_chunk(nvrar_comm_t comm, size_t bytes);

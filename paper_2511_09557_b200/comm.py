@@ -463,6 +463,20 @@ def _check_host_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
         raise InvalidArgumentError("nvrar: buffers must be contiguous")
 
 
+def _check_uniform(inputs: Sequence[torch.Tensor], outputs: Sequence[torch.Tensor],
+                   device: Optional[int] = None) -> None:
+    """One launch covers every virtual rank with inputs[0]'s length and dtype,
+    so every buffer must have them (a shorter one would be read or written past
+    its end) and, for device buffers, live on the group's device."""
+    n, dt = inputs[0].numel(), inputs[0].dtype
+    for t in list(inputs) + list(outputs):
+        if t.numel() != n or t.dtype != dt:
+            raise InvalidArgumentError("nvrar: every rank's buffers must have the same length "
+                                       "and dtype")
+        if device is not None and t.is_cuda and t.device.index != device:
+            raise InvalidArgumentError(f"nvrar: buffer on {t.device}, group is on cuda:{device}")
+
+
 def _check_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
     if send.numel() != recv.numel():
         raise InvalidArgumentError("nvrar: input and output lengths differ")
@@ -582,6 +596,7 @@ class LocalGroup:
             raise InvalidArgumentError("one input and one output per rank")
         for a, b in zip(inputs, outputs):
             _check_host_pair(a, b)
+        _check_uniform(inputs, outputs)
         send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
         recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])
         rc = self._lib.nvrar_allreduce_local_host(self._arr, p, send, recv, inputs[0].numel(),
@@ -609,14 +624,18 @@ class LocalGroup:
             raise InvalidArgumentError("one input and one output per rank")
         for a, b in zip(inputs, outputs):
             _check_pair(a, b)
+        _check_uniform(inputs, outputs, self.device)
         n = inputs[0].numel()
         dt = dtype_code(inputs[0].dtype)
         send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
         recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])
         mask = (1 << 64) - 1 if active is None else sum(1 << r for r in active)
         if residuals is not None:
+            if len(residuals) != p:
+                raise InvalidArgumentError("one residual per rank")
             for x in residuals:
                 _check_pair(inputs[0], x)
+            _check_uniform(inputs, residuals, self.device)
             res = (ctypes.c_void_p * p)(*[t.data_ptr() for t in residuals])
             rc = self._lib.nvrar_allreduce_local_residual(self._arr, p, send, recv, res, n, dt,
                                                           L.SUM, _stream_ptr(stream), mask)
@@ -656,6 +675,8 @@ class LocalGroup:
             raise InvalidArgumentError("one input and one output per rank")
         for a, b in zip(inputs, outputs):
             _check_phase_io(code, a, b, self.topo.gpus_per_node)
+        _check_uniform(inputs, [], self.device)
+        _check_uniform(outputs, [], self.device)
         dt = dtype_code(dtype if code == PHASE_RD_INTER else inputs[0].dtype)
         send = (ctypes.c_void_p * p)(*[t.data_ptr() for t in inputs])
         recv = (ctypes.c_void_p * p)(*[t.data_ptr() for t in outputs])

@@ -232,11 +232,14 @@ void plan_shape(int world, int nodes, int gpus, int algo_pref, int blocks_pref, 
   }
   if (a == NVRAR_ALGO_AUTO) a = da;
   if (b <= 0) b = da == a ? db : std::max(db, 16);
-  if ((a == NVRAR_ALGO_TWOSHOT || a == NVRAR_ALGO_ONESHOT) && !flat_ok) a = NVRAR_ALGO_HIER;
   if ((a == NVRAR_ALGO_ONESHOT || a == NVRAR_ALGO_MCAST) && bytes > kOneshotMaxBytes) {
     a = NVRAR_ALGO_TWOSHOT;
   }
-  if (a == NVRAR_ALGO_MCAST && !flat_ok) a = NVRAR_ALGO_HIER;
+  // after the size rewrite: a flat schedule on a topology its register tile
+  // cannot hold runs the hierarchical kernel
+  if ((a == NVRAR_ALGO_TWOSHOT || a == NVRAR_ALGO_ONESHOT || a == NVRAR_ALGO_MCAST) && !flat_ok) {
+    a = NVRAR_ALGO_HIER;
+  }
   if (a == NVRAR_ALGO_DIRECT && !emu) a = NVRAR_ALGO_HIER;
   b = std::max(1, std::min(b, max_ctas));
   *algo = a;
@@ -695,6 +698,11 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   if (count == 0 && (phase == NVRAR_PHASE_REDUCE_SCATTER || phase == NVRAR_PHASE_ALL_GATHER)) {
     return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "intra phase: bad vector length 0");
   }
+  // the order frame (shard index, window offsets) is 32-bit in the flat and
+  // direct kernels: whole vectors stay below 2^31 elements
+  if ((n_order ? n_order : count) >= (1ull << 31)) {
+    return fail(c0, NVRAR_ERR_INVALID_ARGUMENT, "nvrar: vectors of 2^31 or more elements are not supported");
+  }
   LaunchParams lp{};
   int nl = 0;
   for (int i = 0; i < ncomms; ++i) {
@@ -1126,20 +1134,20 @@ const int kHostUnitsPerThread = [] {
   return v >= 1 && v <= 64 ? v : 8;
 }();
 
-// Chunk of the host pipeline (bytes per rank): NVRAR_HOST_CHUNK if set; else
-// the whole vector while all local ranks move <= 4 MB (measured: the copies'
-// per-launch and cross-stream costs eat the overlap at 1 MB per rank — P=2
-// 65 us unchunked vs 87 us in 256 KB chunks), above that max(512 KB, 1/4 of
-// the vector). A function of (count, dtype, local ranks) only: ranks agree.
-size_t host_chunk_bytes(const nvrar_comm* c, size_t rank_bytes, int nc) {
+// Window of the host path (bytes per rank): nvrar_set_host_chunk or
+// NVRAR_HOST_CHUNK if set, else the whole vector (one launch; only vectors
+// longer than the comm's max_bytes are split). A function of (count, dtype,
+// knobs) only, so every rank issues the same launches. (Measured at <= 4 MB:
+// the copies' per-launch and cross-stream costs eat the overlap of a chunked
+// pipeline — P=2 1 MB 65 us whole vs 87 us in 256 KB chunks.)
+size_t host_chunk_bytes(const nvrar_comm* c, size_t rank_bytes) {
   static const long long env = [] {
     const char* e = getenv("NVRAR_HOST_CHUNK");
     return e ? atoll(e) : 0LL;
   }();
   if (c->host_chunk) return c->host_chunk;
   if (env >= 4096) return static_cast<size_t>(env);
-  if (rank_bytes * static_cast<size_t>(nc) <= (4u << 20)) return std::max<size_t>(rank_bytes, 16);
-  return std::max<size_t>(512 << 10, rank_bytes / 4);
+  return std::max<size_t>(rank_bytes, 16);
 }
 
 int host_pipe_ready(nvrar_comm* c, size_t chunk) {
@@ -1191,44 +1199,37 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
     zsend[r] = a.devicePointer;
     zrecv[r] = b.devicePointer;
   }
-  if (mapped && !c0->host_chunk) {
-    if (count * eb <= c0->max_bytes) {
-      return launch(comms, nc, zsend.data(), zrecv.data(), count, dtype, op, stream, ~0ull,
-                    local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr, 0, 0,
-                    kHostUnitsPerThread);
-    }
-    // longer than the staging the comm was sized for: windows of the whole
-    // vector straight over the mapped host memory (same bits as one call)
-    if (c0->world > 16 || c0->gpus > flat_max_gpus(c0->nodes)) {
-      return fail(c0, NVRAR_ERR_INVALID_ARGUMENT,
-                  "nvrar: vector longer than the preallocated maximum (%zu B > %zu B)",
-                  count * eb, c0->max_bytes);
-    }
-    const size_t we = c0->max_bytes / eb / 16 * 16;  // window elements, unit aligned
-    std::vector<const void*> ws(nc);
-    std::vector<void*> wr(nc);
-    for (size_t off = 0; off < count; off += we) {
-      const size_t cnt = std::min(we, count - off);
-      for (int r = 0; r < nc; ++r) {
-        ws[r] = static_cast<const uint8_t*>(zsend[r]) + off * eb;
-        wr[r] = static_cast<uint8_t*>(zrecv[r]) + off * eb;
-      }
-      if (int rc = launch(comms, nc, ws.data(), wr.data(), cnt, dtype, op, stream, ~0ull,
-                          local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr, off, count,
-                          kHostUnitsPerThread)) {
-        return rc;
-      }
-    }
-    return NVRAR_SUCCESS;
-  }
+  // The window schedule is a function of (count, dtype, max_bytes, host chunk)
+  // only — never of the memory kind — so every rank issues the
+  // same sequence of launches whether its buffers are pinned or pageable.
   // units of 16 bytes, so every window starts on a unit boundary
   const size_t chunk_elems =
-      std::max<size_t>(16 / eb, (host_chunk_bytes(c0, count * eb, nc) + 15) / 16 * 16 / eb);
+      std::max<size_t>(16 / eb, (host_chunk_bytes(c0, count * eb) + 15) / 16 * 16 / eb);
   const bool windows = c0->world <= 16 && c0->gpus <= flat_max_gpus(c0->nodes);
   // a window never exceeds what the comm's staging was sized for
   const size_t ce = windows ? std::min(chunk_elems, std::max<size_t>(16 / eb,
                                                                     c0->max_bytes / eb / 16 * 16))
                             : std::max<size_t>(count, 1);
+  const size_t nch = count == 0 ? 1 : (count + ce - 1) / ce;
+  if (mapped && !c0->host_chunk) {
+    // zero-copy (unless a chunk was asked for, which means staging): the same
+    // windows, straight over the mapped host memory
+    std::vector<const void*> ws(nc);
+    std::vector<void*> wr(nc);
+    for (size_t i = 0; i < nch; ++i) {
+      const size_t off = i * ce, cnt = std::min(ce, count - off);
+      for (int r = 0; r < nc; ++r) {
+        ws[r] = static_cast<const uint8_t*>(zsend[r]) + off * eb;
+        wr[r] = static_cast<uint8_t*>(zrecv[r]) + off * eb;
+      }
+      if (int rc = launch(comms, nc, ws.data(), wr.data(), cnt, dtype, op, stream, ~0ull,
+                          local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr,
+                          nch > 1 ? off : 0, nch > 1 ? count : 0, kHostUnitsPerThread)) {
+        return rc;
+      }
+    }
+    return NVRAR_SUCCESS;
+  }
   const size_t chunk = std::max<size_t>(ce * eb, 16);
   for (int i = 0; i < nc; ++i) {
     if (int rc = host_pipe_ready(comms[i], chunk)) return rc;
@@ -1239,7 +1240,6 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
     return launch(comms, nc, hsend, const_cast<void* const*>(hrecv), 0, dtype, op, stream,
                   ~0ull, local_group);
   }
-  const size_t nch = (count + ce - 1) / ce;
   std::vector<const void*> dsend(nc);
   std::vector<void*> drecv(nc);
   if (nch == 1) {

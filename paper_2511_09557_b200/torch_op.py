@@ -12,6 +12,7 @@ call counter lives on the device and advances on every replay. The fake
 """
 from __future__ import annotations
 
+import itertools
 from typing import Dict
 
 import torch
@@ -19,11 +20,12 @@ import torch
 from .comm import Communicator
 
 _COMMS: Dict[int, Communicator] = {}
+_IDS = itertools.count(1)  # never reused: an unregistered id stays dead
 
 
 def register(comm: Communicator) -> int:
     """Make `comm` addressable from the op; returns its id."""
-    cid = len(_COMMS) + 1
+    cid = next(_IDS)
     _COMMS[cid] = comm
     return cid
 

@@ -142,6 +142,37 @@ def torch_ops(comm, rank, nodes, gpus, device, log):
     return fails
 
 
+def host_mixed(comm, rank, nodes, gpus, log):
+    """nvrar_allreduce_host with even ranks on pinned (zero-copy) and odd ranks
+    on pageable (staged) memory: the window schedule must not depend on the
+    memory kind (a vector longer than max_bytes -> several windows; then an
+    explicit host chunk)."""
+    world = nodes * gpus
+    fails = 0
+    for chunk in (0, 256 << 10):
+        comm.set_host_chunk(chunk)
+        for dtype in ("f32", "bf16"):
+            n = 700001
+            x = _inputs(dtype, world, n, 620)
+            t = torch.from_numpy(np.ascontiguousarray(x[rank]))
+            if dtype == "bf16":
+                t = t.view(torch.int16).view(torch.bfloat16)
+            out = torch.empty_like(t)
+            if rank % 2 == 0:
+                t, out = t.pin_memory(), out.pin_memory()
+            comm.allreduce_host(t, out)
+            torch.cuda.synchronize()
+            comm.check()
+            got = out.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" \
+                else out.numpy().view(np.uint32)
+            if not np.array_equal(got, _want(x, nodes, gpus, dtype)):
+                fails += 1
+                log(f"host path ({'pinned' if rank % 2 == 0 else 'pageable'}, chunk {chunk}) "
+                    f"{dtype} differs")
+    comm.set_host_chunk(0)
+    return fails
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dir", required=True)
@@ -152,6 +183,8 @@ def main():
     ap.add_argument("--quick", action="store_true", help="fewer sizes and dtypes")
     ap.add_argument("--ops", action="store_true", help="also the torch.ops.nvrar entry points")
     ap.add_argument("--mismatch", action="store_true", help="length-mismatch protocol fault")
+    ap.add_argument("--host", action="store_true",
+                    help="host-buffer path, pinned on even ranks and pageable on odd ranks")
     ap.add_argument("--timeout", type=float, default=60.0)
     args = ap.parse_args()
     rank = args.rank
@@ -181,6 +214,8 @@ def main():
     dtypes = ("f32", "bf16") if args.quick else ("f32", "bf16", "i32")
     sizes = (4099,) if args.quick else (1, 4099, 65539)
     fails = parity(comm, rank, args.nodes, args.gpus, device, algos, dtypes, sizes, log)
+    if args.host:
+        fails += host_mixed(comm, rank, args.nodes, args.gpus, log)
     if args.ops:
         fails += torch_ops(comm, rank, args.nodes, args.gpus, device, log)
     seq = comm.sequence()

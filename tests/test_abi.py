@@ -134,3 +134,37 @@ def test_host_buffer_argument_checks():
         _check_host_pair(a, torch.zeros(16, dtype=torch.bfloat16))
     with pytest.raises(InvalidArgumentError):
         _check_host_pair(torch.zeros(32)[::2], torch.zeros(16))
+
+
+def test_flat_fallback_applies_after_the_oneshot_size_rewrite():
+    """a >1 MB multicast / one-shot request on a topology the flat
+    kernels cannot hold (32 ranks) must run the hierarchy, not a two-shot that
+    has no kernel."""
+    big = (2 << 20) // 2
+    for algo in (L.ALGO_MCAST, L.ALGO_ONESHOT, L.ALGO_TWOSHOT):
+        assert plan_for(32, 4, 8, big, L.BF16, algo=algo)[0] == "hier"
+
+
+def test_local_group_buffers_must_be_uniform():
+    """one launch covers every virtual rank with inputs[0]'s length
+    and dtype, so a shorter or differently typed buffer is rejected."""
+    import torch
+    from paper_2511_09557_b200.comm import InvalidArgumentError, _check_uniform
+    a = [torch.zeros(16) for _ in range(4)]
+    _check_uniform(a, [torch.zeros(16) for _ in range(4)])
+    with pytest.raises(InvalidArgumentError):
+        _check_uniform(a, [torch.zeros(16)] * 3 + [torch.zeros(15)])
+    with pytest.raises(InvalidArgumentError):
+        _check_uniform(a[:3] + [torch.zeros(16, dtype=torch.bfloat16)], a)
+
+
+def test_torch_op_ids_are_never_reused():
+    """unregister + register must not hand out a live id again."""
+    from paper_2511_09557_b200 import torch_op
+    a = torch_op.register(object())
+    b = torch_op.register(object())
+    torch_op.unregister(a)
+    c = torch_op.register(object())
+    assert len({a, b, c}) == 3
+    torch_op.unregister(b)
+    torch_op.unregister(c)

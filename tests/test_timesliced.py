@@ -82,3 +82,13 @@ def test_timesliced_length_mismatch(nodes, gpus):
     rcs, out = run_ranks(nodes, gpus, ("--mismatch", "--timeout", "5"))
     assert all(rc == 0 for rc in rcs), out[-4000:]
     assert "status 4" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("nodes,gpus", [(2, 1), (1, 2)])
+def test_timesliced_host_path_mixed_memory(nodes, gpus):
+    """one rank with pinned host buffers (zero-copy), the other with
+    pageable ones (staged), vectors longer than max_bytes: both issue the same
+    windows, so the call completes and the bits equal the oracle's."""
+    rcs, out = run_ranks(nodes, gpus, ("--quick", "--host"))
+    assert all(rc == 0 for rc in rcs), out[-4000:]
+    assert out.count(": OK") == nodes * gpus, out[-4000:]
