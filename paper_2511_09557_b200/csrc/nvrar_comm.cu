@@ -204,8 +204,12 @@ void default_plan(int world, int nodes, uint64_t bytes, bool emu, int* algo, int
     *algo = NVRAR_ALGO_DIRECT;
   } else if (bytes <= one_max) {
     *algo = NVRAR_ALGO_ONESHOT;
-  } else if (bytes <= (2u << 20) && nodes > 1 && world >= 8) {
-    // P <= 4: two-shot measured faster than the hierarchy above one_max
+  } else if (bytes <= (1u << 20) && nodes > 1 && world >= 8) {
+    // the hierarchy where the P=4 sweep measured it ahead of both flat
+    // schedules (1 MB: 8.9 vs one-shot 9.2 / two-shot 10.7 us); at 2 MB it was
+    // level with two-shot and behind above (its bf16 RD partials travel as fp32
+    // cells). Unmeasured at P=8 here: bench.py / selector.autotune replace this
+    // row with the measured table on the running box.
     *algo = NVRAR_ALGO_HIER;
   } else {
     *algo = NVRAR_ALGO_TWOSHOT;

@@ -74,7 +74,10 @@ class TpDecodeSkeleton:
     """One rank's share of a Llama decode step (see the module docstring)."""
 
     def __init__(self, model: str, batch: int, tp: int, device: torch.device,
-                 weight_sets: int = 2, seed: int = 0, layers: int | None = None):
+                 weight_sets: int = 2, seed: int = 0, layers: int | None = None,
+                 weight_seed: int | None = None):
+        """seed: the replicated residual stream x0 (same on every rank);
+        weight_seed: this rank's weight shards (default: seed)."""
         cfg = LLAMA[model]
         h, ffn = cfg["hidden"], cfg["ffn"]
         hd = h // cfg["heads"]
@@ -84,7 +87,7 @@ class TpDecodeSkeleton:
         self.layers = layers or cfg["layers"]
         qkv = (cfg["heads"] + 2 * cfg["kv_heads"]) * hd // tp
         g = torch.Generator(device=device)
-        g.manual_seed(seed)
+        g.manual_seed(seed if weight_seed is None else weight_seed)
 
         def w(r, c):
             return (torch.randn(r, c, device=device, generator=g, dtype=torch.float32)
@@ -92,7 +95,9 @@ class TpDecodeSkeleton:
 
         self.sets = [dict(qkv=w(h, qkv), o=w(h // tp, h), gu=w(h, 2 * ffn // tp),
                           down=w(ffn // tp, h)) for _ in range(weight_sets)]
-        self.x0 = (torch.randn(batch, h, device=device, generator=g) * 0.1).to(torch.bfloat16)
+        gx = torch.Generator(device=device)
+        gx.manual_seed(seed)
+        self.x0 = (torch.randn(batch, h, device=device, generator=gx) * 0.1).to(torch.bfloat16)
         self.x = self.x0.clone()
         self.ffn_shard = ffn // tp
 
@@ -122,6 +127,46 @@ class TpDecodeSkeleton:
             gu = F.rms_norm(x, (self.hidden,)) @ W["gu"]
             add_reduced((F.silu(gu[:, :self.ffn_shard]) * gu[:, self.ffn_shard:]) @ W["down"])
         self.out = x
+
+
+def bf16_ulp(v: torch.Tensor) -> torch.Tensor:
+    """Spacing of bf16 numbers at |v| (8 significant bits), as fp32."""
+    a = v.abs().float().clamp_min(2.0 ** -126)
+    return torch.exp2(torch.floor(torch.log2(a)) - 7)
+
+
+def check_allreduce(a: torch.Tensor, all_reduce, nccl_all_reduce) -> dict:
+    """The all-reduce a decode layer produces, checked on real per-rank data:
+    every rank's activation `a` is gathered, the exact fp32 sum taken in rank
+    order, and (1) NVRAR's bf16 result must be within 1 bf16 ulp of it (fp32
+    partials, one final RNE: the only difference to the fp32 sum is that
+    rounding plus fp32 reassociation), (2) NCCL's within the SURVEY §8c bound
+    h * 2^-8 * sum_r |x_r| with h = P - 1 bf16 roundings on its path."""
+    import torch.distributed as dist
+    P = dist.get_world_size()
+    parts = [torch.empty_like(a) for _ in range(P)]
+    dist.all_gather(parts, a)
+    ref = torch.zeros_like(a, dtype=torch.float32)
+    absum = torch.zeros_like(ref)
+    for t in parts:
+        ref += t.float()
+        absum += t.float().abs()
+    nv = a.clone()
+    all_reduce(nv)
+    nc = a.clone()
+    nccl_all_reduce(nc)
+    torch.cuda.synchronize()
+    nv_ulps = float(((nv.float() - ref).abs() / bf16_ulp(ref)).max())
+    bound = max(P - 1, 1) * 2.0 ** -8 * absum
+    nc_ratio = float(((nc.float() - ref).abs() / bound.clamp_min(1e-30)).max())
+    nv_vs_nc = float((nv.float() - nc.float()).abs().max())
+    res = {"nvrar_max_ulp_vs_fp32_sum": round(nv_ulps, 3),
+           "nccl_max_err_over_bound": round(nc_ratio, 4),
+           "nvrar_vs_nccl_max_abs": nv_vs_nc,
+           "inputs_differ_across_ranks": bool(any(not torch.equal(parts[0], t)
+                                                  for t in parts[1:]))}
+    res["ok"] = bool(nv_ulps <= 1.0 and nc_ratio <= 1.0 and res["inputs_differ_across_ranks"])
+    return res
 
 
 def _graph(fn, warmup: int = 2) -> torch.cuda.CUDAGraph:
@@ -199,8 +244,15 @@ def main() -> None:
 
     for batch in batches:
         wl = DecodeWorkload(batch, cfg["hidden"], 2, args.layers or cfg["layers"])
+        # per-rank weights and activations (each rank holds a different shard):
+        # the all-reduces sum P different tensors
         m = TpDecodeSkeleton(args.model, batch, tp, torch.device("cuda", local),
-                             layers=args.layers or None)
+                             layers=args.layers or None, seed=0,
+                             weight_seed=1000 + rank)
+        W0 = m.sets[0]
+        qkv0 = F.rms_norm(m.x0, (m.hidden,)) @ W0["qkv"]
+        a0 = (qkv0[:, :m.hidden // tp] @ W0["o"]).contiguous()
+        ar_check = check_allreduce(a0, nvrar_ar, nccl_ar)
         res = {}
         outs = {}
         for name, ar, fu in (("nvrar", nvrar_ar, None), ("nvrar_fused", None, nvrar_fused),
@@ -211,7 +263,8 @@ def main() -> None:
             outs[name] = m.out.float().clone()
             del gr
         comm.check()
-        # both collectives must give the same model output (bf16 sums, different orders)
+        # the two arms' model outputs differ only by bf16 rounding (different
+        # reduction orders over 160/252 all-reduces); reported, not asserted
         diff = float((outs["nvrar"] - outs["nccl"]).abs().max())
         # the fused epilogue must reproduce the unfused NVRAR step bit for bit
         fused_equal = bool(torch.equal(outs["nvrar"], outs["nvrar_fused"]))
@@ -230,7 +283,8 @@ def main() -> None:
                 "fused_step_speedup_vs_nccl": round(res["nccl"] / res["nvrar_fused"], 4),
                 "fused_bit_identical": fused_equal,
                 "weight_mb_per_layer": round(m.weight_bytes_per_layer() / 2**20, 1),
-                "max_abs_diff_vs_nccl": diff, "out_scale": scale,
+                "allreduce_check": ar_check,
+                "model_out_max_abs_diff_vs_nccl": diff, "out_scale": scale,
                 "timing": "CUDA graph of one full step, CUDA events, max over ranks, median",
             }), flush=True)
         del m

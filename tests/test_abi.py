@@ -112,6 +112,7 @@ def test_selector_default_policy_and_fallbacks():
     # the paper's hierarchy in the middle at P = 8
     assert plan_for(8, 2, 4, (1 << 20) // 2, L.BF16)[0] == "hier"
     assert plan_for(8, 2, 4, (8 << 20) // 2, L.BF16)[0] == "twoshot"
+    assert plan_for(8, 2, 4, (2 << 20) // 2, L.BF16)[0] == "twoshot"
     # single rank: a copy through the one-shot
     assert plan_for(1, 1, 1, 1000, L.FLOAT32)[0] == "oneshot"
     # multicast one-shot: bounded like the one-shot; hierarchy where flat is not allowed
