@@ -11,7 +11,9 @@
  *   NvrarAllreduce<T>(Ctx&, max_elems)  nvrar.hpp:44-78  | nvrar_init / nvrar_comm_create
  *     + ClusterTopology{nodes,gpus}     topology.hpp:24-48 |   + nvrar_comm_export
  *     + Ctx::alloc_region (symmetric)   transport.hpp:146-148 |   + nvrar_comm_connect
- *   Ctx::alloc_region for caller data   transport.hpp:146-148 | nvrar_alloc_symmetric
+ *   Ctx::alloc_region for caller data   transport.hpp:146-148 | nvrar_alloc_symmetric,
+ *                                                        |   nvrar_register_buffer +
+ *                                                        |   nvrar_connect_buffer
  *   NvrarAllreduce<T>::run(in,out,cfg)  nvrar.hpp:84-129 | nvrar_allreduce
  *   NvrarConfig{blocks,chunk_bytes}     fused.hpp:106-116 | nvrar_set_config
  *   NvrarAllreduce<T>::sequence()       nvrar.hpp:80     | nvrar_get_sequence
@@ -158,14 +160,42 @@ int nvrar_comm_export(nvrar_comm_t comm, nvrar_handle_t* handle);
 int nvrar_comm_connect(nvrar_comm_t comm, const nvrar_handle_t* handles, int count);
 int nvrar_finalize(nvrar_comm_t comm);
 
-/* Symmetric caller buffer from the comm's own allocator (Ctx::alloc_region
- * analogue): every rank must call it in the same order with the same size.
- * The memory is zeroed and freed by nvrar_finalize. */
+/* ---- buffer registration (Ctx::alloc_region's symmetric regions for caller
+ * data, transport.hpp:146-148) ---------------------------------
+ * A caller's device buffer becomes peer-accessible in two steps, so the host
+ * can use any bootstrap: nvrar_register_buffer exports this rank's range
+ * (any range inside a cudaMalloc allocation) as an opaque handle and returns
+ * its id; after an all-gather of the handles, nvrar_connect_buffer maps every
+ * peer's range (CUDA IPC; same-process ranks directly). Symmetric: every rank
+ * registers the same number of bytes, in the same order (ids then agree).
+ * Registered inputs can be all-reduced in place (nvrar_allreduce_registered);
+ * nvrar_buffer_peer_ptr gives the caller peer rank p's range as mapped here.
+ * nvrar_deregister_buffer (not collective; synchronises the device) unmaps.
+ * The caller keeps registered memory alive until it deregisters or finalizes. */
+int nvrar_register_buffer(nvrar_comm_t comm, void* dev_ptr, size_t bytes,
+                          nvrar_handle_t* handle, int* buf);
+int nvrar_connect_buffer(nvrar_comm_t comm, int buf, const nvrar_handle_t* handles, int count);
+int nvrar_deregister_buffer(nvrar_comm_t comm, int buf);
+int nvrar_buffer_peer_ptr(nvrar_comm_t comm, int buf, int peer, void** ptr);
+/* Symmetric allocation (Ctx::alloc_region itself): collective — every rank
+ * calls it in the same order with the same size; the memory is zeroed,
+ * registered and connected through the allgather callback the comm was
+ * created with (nvrar_init; a comm from nvrar_comm_create has none and gets
+ * INVALID_ARGUMENT), and freed by nvrar_finalize. */
 int nvrar_alloc_symmetric(nvrar_comm_t comm, size_t bytes, void** dev_ptr);
 
 /* ---- the collective ----------------------------------------------------- */
 int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t count,
                     nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
+
+/* All-reduce whose INPUT lies in a registered, connected buffer (at the same
+ * offset on every rank): no staging — every rank reads its peers' inputs in
+ * place over NVLink and folds them in the reference order (same bits as
+ * nvrar_allreduce). The launch completes only after every peer has finished
+ * reading this rank's input, so the caller may overwrite it right after.
+ * Consumes one sequence number like any call; world <= 32. */
+int nvrar_allreduce_registered(nvrar_comm_t comm, const void* send, void* recv, size_t count,
+                               nvrar_dtype_t dtype, nvrar_op_t op, void* stream);
 
 /* All ranks that live on ONE device (virtual ranks sharing a GPU) in ONE
  * launch: cooperative when the schedule makes ranks wait on each other (so

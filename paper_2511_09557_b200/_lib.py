@@ -86,6 +86,13 @@ SIGNATURES = {
     "nvrar_comm_connect": (_c.c_int, [_vp, _c.POINTER(Handle), _c.c_int]),
     "nvrar_finalize": (_c.c_int, [_vp]),
     "nvrar_alloc_symmetric": (_c.c_int, [_vp, _c.c_size_t, _c.POINTER(_vp)]),
+    "nvrar_register_buffer": (_c.c_int, [_vp, _vp, _c.c_size_t, _c.POINTER(Handle),
+                                         _c.POINTER(_c.c_int)]),
+    "nvrar_connect_buffer": (_c.c_int, [_vp, _c.c_int, _c.POINTER(Handle), _c.c_int]),
+    "nvrar_deregister_buffer": (_c.c_int, [_vp, _c.c_int]),
+    "nvrar_buffer_peer_ptr": (_c.c_int, [_vp, _c.c_int, _c.c_int, _c.POINTER(_vp)]),
+    "nvrar_allreduce_registered": (_c.c_int, [_vp, _vp, _vp, _c.c_size_t, _c.c_int, _c.c_int,
+                                              _vp]),
     "nvrar_allreduce": (_c.c_int, [_vp, _vp, _vp, _c.c_size_t, _c.c_int, _c.c_int, _vp]),
     "nvrar_allreduce_local": (_c.c_int, [_c.POINTER(_vp), _c.c_int, _c.POINTER(_vp),
                                          _c.POINTER(_vp), _c.c_size_t, _c.c_int, _c.c_int, _vp,

@@ -46,6 +46,7 @@ def communicator_from_dir(path: str, topo: ClusterTopology, rank: int, max_bytes
     if not 0 <= rank < topo.world_size():
         raise InvalidArgumentError(f"rank {rank} out of range")
     comm = Communicator(topo, rank, device, max_bytes, **kw)
-    handles = file_allgather(path, rank, topo.world_size(), comm.export())
-    comm.connect(handles)
+    world = topo.world_size()
+    comm.exchange = lambda blob, tag: file_allgather(path, rank, world, blob, tag=tag)
+    comm.connect(comm.exchange(comm.export(), "h"))
     return comm

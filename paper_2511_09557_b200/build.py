@@ -16,7 +16,8 @@ LIB_DIR = os.environ.get("NVRAR_BUILD_DIR") or os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libnvrar_b200.so")
 SOURCES = ["nvrar_inst_f32.cu", "nvrar_inst_bf16.cu", "nvrar_inst_i32.cu",
            "nvrar_flat_f32.cu", "nvrar_flat_bf16.cu", "nvrar_flat_i32.cu",
-           "nvrar_inst_phase_f.cu", "nvrar_inst_phase_i.cu", "nvrar_misc.cu", "nvrar_comm.cu"]
+           "nvrar_inst_phase_f.cu", "nvrar_inst_phase_i.cu", "nvrar_pull.cu", "nvrar_misc.cu",
+           "nvrar_comm.cu"]
 HEADERS = ["nvrar_device.cuh", "nvrar_kernels.cuh", os.path.join("..", "..", "include", "nvrar.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

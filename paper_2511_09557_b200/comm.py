@@ -233,10 +233,8 @@ class Communicator:
         if device is None:
             device = torch.cuda.current_device()
         comm = cls(topo, rank, device, max_bytes, **kw)
-        mine = comm.export()
-        allh: List[Optional[bytes]] = [None] * dist.get_world_size(group)
-        dist.all_gather_object(allh, mine, group=group)
-        comm.connect(allh)  # type: ignore[arg-type]
+        comm.exchange = lambda blob, tag: _dist_allgather(blob, group)
+        comm.connect(comm.exchange(comm.export(), "comm"))
         return comm
 
     def enable_multicast(self, group=None) -> bool:
@@ -283,6 +281,57 @@ class Communicator:
         t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
         return bool(t.item())
+
+    # -- registered buffers (nvrar_register_buffer, include/nvrar.h) ------------
+    # `exchange(blob, tag) -> [blob per rank]` is the bootstrap all-gather the
+    # comm was connected with (torch.distributed, or a shared directory)
+    exchange = None
+
+    def register_buffer(self, t: torch.Tensor) -> int:
+        """Register `t` (a CUDA tensor, same size on every rank, registered in
+        the same order) and map every peer's; collective. Returns the id."""
+        if not (t.is_cuda and t.is_contiguous()):
+            raise InvalidArgumentError("nvrar: registered buffers are contiguous CUDA tensors")
+        if self.exchange is None:
+            raise InvalidArgumentError("nvrar: this communicator has no bootstrap exchange")
+        hd = L.Handle()
+        buf = ctypes.c_int()
+        self._check(self._lib.nvrar_register_buffer(self._h, t.data_ptr(),
+                                                    t.numel() * t.element_size(),
+                                                    ctypes.byref(hd), ctypes.byref(buf)))
+        allh = self.exchange(bytes(hd.bytes), f"reg{buf.value}")
+        arr = (L.Handle * len(allh))()
+        for i, b in enumerate(allh):
+            ctypes.memmove(arr[i].bytes, b, L.HANDLE_BYTES)
+        self._check(self._lib.nvrar_connect_buffer(self._h, buf.value, arr, len(allh)))
+        self._registered = getattr(self, "_registered", {})
+        self._registered[buf.value] = t  # keep the memory alive while registered
+        return buf.value
+
+    def alloc_symmetric(self, numel: int, dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+        """A zeroed tensor registered with the comm (Ctx::alloc_region for caller
+        data, transport.hpp:146-148); collective."""
+        t = torch.zeros(numel, dtype=dtype, device=f"cuda:{self.device}")
+        self.register_buffer(t)
+        return t
+
+    def deregister_buffer(self, buf: int) -> None:
+        self._check(self._lib.nvrar_deregister_buffer(self._h, buf))
+        getattr(self, "_registered", {}).pop(buf, None)
+
+    def buffer_peer_ptr(self, buf: int, peer: int) -> int:
+        p = ctypes.c_void_p()
+        self._check(self._lib.nvrar_buffer_peer_ptr(self._h, buf, peer, ctypes.byref(p)))
+        return int(p.value or 0)
+
+    def allreduce_registered(self, send: torch.Tensor, recv: torch.Tensor,
+                             stream: Optional[torch.cuda.Stream] = None) -> None:
+        """nvrar_allreduce_registered: `send` inside a registered buffer (same
+        offset on every rank); peers' inputs are read in place."""
+        _check_pair(send, recv)
+        self._check(self._lib.nvrar_allreduce_registered(
+            self._h, send.data_ptr(), recv.data_ptr(), send.numel(), dtype_code(send.dtype),
+            L.SUM, _stream_ptr(stream)))
 
     # -- knobs / introspection --------------------------------------------------
     def set_config(self, cfg: NvrarConfig) -> None:
@@ -445,6 +494,13 @@ class Communicator:
     def _check(self, rc: int) -> None:
         if rc:
             _raise(rc, self.last_error(), self.rank)
+
+
+def _dist_allgather(blob: bytes, group=None) -> List[bytes]:
+    import torch.distributed as dist
+    out: List[Optional[bytes]] = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(blob), group=group)
+    return [bytes(b) for b in out]  # type: ignore[arg-type]
 
 
 def _blocked_rank(b: L.Blocked) -> BlockedRank:

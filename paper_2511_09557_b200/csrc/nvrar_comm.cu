@@ -22,6 +22,7 @@ KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool
 KernelFn bump_kernel();
 KernelFn select_direct(int dtype, int nodes, int gpus);
 KernelFn select_phase(int dtype, int mode, int nodes, bool emu);
+KernelFn select_pull(int dtype, int nodes, int gpus);
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);
 PingFn pingpong_fn();
 int flat_max_gpus(int nodes);
@@ -71,7 +72,21 @@ struct nvrar_comm {
   RankDesc* d_desc = nullptr;
   RankDesc h_desc{};
   std::vector<uint8_t*> opened;  // IPC mappings to close
-  std::vector<void*> sym_allocs;
+  // caller buffers registered with the comm (nvrar_register_buffer): this
+  // rank's range and every peer's mapping of its own registration
+  struct RegBuf {
+    int id = 0;
+    uint8_t* local = nullptr;
+    size_t bytes = 0;
+    bool owned = false;      // nvrar_alloc_symmetric memory, freed with the registration
+    bool connected = false;
+    uint8_t* peer[kMaxRanks] = {};
+    std::vector<uint8_t*> opened;
+  };
+  std::vector<RegBuf> regs;
+  int next_reg = 1;
+  nvrar_allgather_fn allgather = nullptr;  // nvrar_init's bootstrap (nvrar_alloc_symmetric)
+  void* allgather_ctx = nullptr;
   int blocks = 0;
   uint64_t chunk_bytes = 65536;
   int algo = NVRAR_ALGO_AUTO;
@@ -139,7 +154,9 @@ Layout make_layout(int world, int nodes, int gpus, size_t max_bytes) {
     off += (bytes + 255) & ~255ull;
     return o;
   };
-  l.ctrl_off = take(sizeof(uint64_t) * kMaxRanks);
+  // counters, the ping-pong word and the done words each get their own block
+  // (the ping-pong word once sat past a 64-word block, on the first A slot)
+  l.ctrl_off = take(sizeof(uint64_t) * kCtrlWords);
   // 8-byte words per slot: one per element (8 B/element worst) rounded up to
   // whole 32-unit groups of up to 8 elements.
   auto slot_words = [](uint64_t elems) { return ((elems + 255) & ~255ull) + 256; };
@@ -480,6 +497,8 @@ int nvrar_init(const nvrar_init_args* a, nvrar_comm_t* out) {
     nvrar_finalize(c);
     return rc;
   }
+  c->allgather = a->allgather;
+  c->allgather_ctx = a->allgather_ctx;
   *out = c;
   return NVRAR_SUCCESS;
 }
@@ -506,8 +525,12 @@ int nvrar_finalize(nvrar_comm_t c) {
   cudaDeviceSynchronize();
   mc_teardown(c);
   host_pipe_teardown(c);
+  for (auto& r : c->regs) {
+    for (auto* p : r.opened) cudaIpcCloseMemHandle(p);
+    if (r.owned) cudaFree(r.local);
+  }
+  c->regs.clear();
   for (auto* p : c->opened) cudaIpcCloseMemHandle(p);
-  for (auto* p : c->sym_allocs) cudaFree(p);
   if (c->region) cudaFree(c->region);
   if (c->state) cudaFree(c->state);
   if (c->d_desc) cudaFree(c->d_desc);
@@ -516,13 +539,183 @@ int nvrar_finalize(nvrar_comm_t c) {
   return NVRAR_SUCCESS;
 }
 
+// ---- registered buffers (Ctx::alloc_region's symmetric regions for caller
+// data, transport.hpp:146-148) ------------------------------------------------
+namespace {
+
+constexpr uint32_t kRegMagic = 0x4E565242u;  // "NVRB"
+
+struct RegBlob {
+  uint32_t magic;
+  int32_t pid, device, rank, id;
+  uint64_t base_ptr;  // the allocation's base (what cudaIpcOpenMemHandle maps)
+  uint64_t offset;    // the registered range's offset in it
+  uint64_t bytes;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(RegBlob) <= NVRAR_HANDLE_BYTES, "registration handle too large");
+
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda link)
+int alloc_base(nvrar_comm* c, const void* p, uint8_t** base, size_t* size) {
+  using Fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      f = nullptr;
+    }
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (!fn) return fail(c, NVRAR_ERR_CUDA, "cuMemGetAddressRange is unavailable");
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "buffer %p is not device memory of this process", p);
+  }
+  *base = reinterpret_cast<uint8_t*>(b);
+  *size = sz;
+  return NVRAR_SUCCESS;
+}
+
+nvrar_comm::RegBuf* find_reg(nvrar_comm* c, int id) {
+  for (auto& r : c->regs) {
+    if (r.id == id) return &r;
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+int nvrar_register_buffer(nvrar_comm_t c, void* dev_ptr, size_t bytes, nvrar_handle_t* handle,
+                          int* buf) {
+  if (!c || !dev_ptr || !handle || !buf || bytes == 0) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "register: null argument or empty range");
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  uint8_t* base = nullptr;
+  size_t size = 0;
+  if (int rc = alloc_base(c, dev_ptr, &base, &size)) return rc;
+  const uint8_t* p = static_cast<const uint8_t*>(dev_ptr);
+  if (p + bytes > base + size) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "register: range runs past its allocation");
+  }
+  RegBlob b{};
+  b.magic = kRegMagic;
+  b.pid = static_cast<int32_t>(getpid());
+  b.device = c->device;
+  b.rank = c->rank;
+  b.base_ptr = reinterpret_cast<uint64_t>(base);
+  b.offset = static_cast<uint64_t>(p - base);
+  b.bytes = bytes;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&b.ipc, base));
+  nvrar_comm::RegBuf r;
+  r.id = c->next_reg++;
+  r.local = const_cast<uint8_t*>(p);
+  r.bytes = bytes;
+  b.id = r.id;
+  c->regs.push_back(std::move(r));
+  std::memset(handle->bytes, 0, sizeof(handle->bytes));
+  std::memcpy(handle->bytes, &b, sizeof(b));
+  *buf = b.id;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_connect_buffer(nvrar_comm_t c, int buf, const nvrar_handle_t* hs, int count) {
+  if (!c || !hs) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  nvrar_comm::RegBuf* r = find_reg(c, buf);
+  if (!r) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "no registered buffer %d", buf);
+  if (count != c->world) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "expected %d handles, got %d", c->world, count);
+  }
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int32_t mypid = static_cast<int32_t>(getpid());
+  for (int q = 0; q < count; ++q) {
+    RegBlob b;
+    std::memcpy(&b, hs[q].bytes, sizeof(b));
+    if (b.magic != kRegMagic || b.rank != q) {
+      return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "registration handle %d: bad magic or rank", q);
+    }
+    if (b.bytes != r->bytes) {
+      // symmetric: every rank registers the same size in the same order
+      return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                  "registration %d: rank %d registered %llu bytes, this rank %zu", buf, q,
+                  static_cast<unsigned long long>(b.bytes), r->bytes);
+    }
+    if (q == c->rank) {
+      r->peer[q] = r->local;
+      continue;
+    }
+    if (b.pid == mypid) {
+      r->peer[q] = reinterpret_cast<uint8_t*>(b.base_ptr) + b.offset;
+    } else {
+      void* m = nullptr;
+      CUDA_TRY(c, cudaIpcOpenMemHandle(&m, b.ipc, cudaIpcMemLazyEnablePeerAccess));
+      r->opened.push_back(static_cast<uint8_t*>(m));
+      r->peer[q] = static_cast<uint8_t*>(m) + b.offset;
+    }
+  }
+  r->connected = true;
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_deregister_buffer(nvrar_comm_t c, int buf) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  for (size_t i = 0; i < c->regs.size(); ++i) {
+    if (c->regs[i].id != buf) continue;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    for (auto* p : c->regs[i].opened) cudaIpcCloseMemHandle(p);
+    if (c->regs[i].owned) cudaFree(c->regs[i].local);
+    c->regs.erase(c->regs.begin() + static_cast<long>(i));
+    return NVRAR_SUCCESS;
+  }
+  return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "no registered buffer %d", buf);
+}
+
+int nvrar_buffer_peer_ptr(nvrar_comm_t c, int buf, int peer, void** ptr) {
+  if (!c || !ptr || peer < 0 || peer >= c->world) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad argument");
+  }
+  nvrar_comm::RegBuf* r = find_reg(c, buf);
+  if (!r || !r->connected) {
+    return fail(c, NVRAR_ERR_NOT_CONNECTED, "buffer %d is not registered and connected", buf);
+  }
+  *ptr = r->peer[peer];
+  return NVRAR_SUCCESS;
+}
+
 int nvrar_alloc_symmetric(nvrar_comm_t c, size_t bytes, void** p) {
   if (!c || !p) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  if (!c->allgather) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                "nvrar_alloc_symmetric needs the bootstrap of nvrar_init; a comm from "
+                "nvrar_comm_create registers caller memory with nvrar_register_buffer + "
+                "nvrar_connect_buffer");
+  }
   CUDA_TRY(c, cudaSetDevice(c->device));
+  const size_t sz = std::max<size_t>(bytes, 16);
   void* q = nullptr;
-  CUDA_TRY(c, cudaMalloc(&q, std::max<size_t>(bytes, 16)));
-  CUDA_TRY(c, cudaMemset(q, 0, std::max<size_t>(bytes, 16)));
-  c->sym_allocs.push_back(q);
+  CUDA_TRY(c, cudaMalloc(&q, sz));
+  CUDA_TRY(c, cudaMemset(q, 0, sz));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  nvrar_handle_t mine;
+  int id = 0;
+  if (int rc = nvrar_register_buffer(c, q, sz, &mine, &id)) {
+    cudaFree(q);
+    return rc;
+  }
+  find_reg(c, id)->owned = true;
+  std::vector<nvrar_handle_t> all(c->world);
+  if (c->allgather(c->allgather_ctx, &mine, all.data(), sizeof(nvrar_handle_t)) != 0) {
+    nvrar_deregister_buffer(c, id);
+    return fail(c, NVRAR_ERR_INTERNAL, "bootstrap allgather failed");
+  }
+  if (int rc = nvrar_connect_buffer(c, id, all.data(), c->world)) {
+    const std::string e = c->last_error;
+    nvrar_deregister_buffer(c, id);
+    return fail(c, rc, "%s", e.c_str());
+  }
   *p = q;
   return NVRAR_SUCCESS;
 }
@@ -829,6 +1022,75 @@ int nvrar_allreduce(nvrar_comm_t comm, const void* send, void* recv, size_t coun
   const void* s[1] = {send};
   void* r[1] = {recv};
   return launch(&comm, 1, s, r, count, dtype, op, stream, ~0ull, false);
+}
+
+int nvrar_allreduce_registered(nvrar_comm_t c, const void* send, void* recv, size_t count,
+                               nvrar_dtype_t dtype, nvrar_op_t op, void* stream) {
+  if (!c) return fail(nullptr, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  if (count == 0) {
+    const void* s[1] = {send};
+    void* r[1] = {recv};
+    return launch(&c, 1, s, r, 0, dtype, op, stream, ~0ull, false);
+  }
+  if (op != NVRAR_SUM) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "only SUM is supported");
+  if (dtype < NVRAR_INT32 || dtype > NVRAR_BF16) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  }
+  if (!c->connected) return fail(c, NVRAR_ERR_NOT_CONNECTED, "comm not connected");
+  if (int s = check_sticky(c)) return fail(c, s, "comm is in a failed state: %s", c->last_error.c_str());
+  if (!recv) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null buffer");
+  if (count >= (1ull << 31)) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "nvrar: vectors of 2^31 or more elements are not supported");
+  }
+  if (c->world > kMaxLocal) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "registered all-reduce: at most %d ranks", kMaxLocal);
+  }
+  const size_t bytes = count * dtype_bytes(dtype);
+  const uint8_t* sp = static_cast<const uint8_t*>(send);
+  const nvrar_comm::RegBuf* reg = nullptr;
+  for (const auto& r : c->regs) {
+    if (r.connected && sp >= r.local && sp + bytes <= r.local + r.bytes) {
+      reg = &r;
+      break;
+    }
+  }
+  if (!reg) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT,
+                "registered all-reduce: send (%zu B) is not inside a registered, connected buffer",
+                bytes);
+  }
+  KernelFn k = select_pull(dtype, c->nodes, c->gpus);
+  if (!k) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "registered all-reduce: topology %dx%d unsupported",
+                c->nodes, c->gpus);
+  }
+  LaunchParams lp{};
+  lp.d0 = c->h_desc;
+  lp.nlocal = 1;
+  lp.count = count;
+  const size_t off = static_cast<size_t>(sp - reg->local);
+  for (int q = 0; q < c->world; ++q) lp.send[q] = reg->peer[q] + off;
+  lp.recv[0] = recv;
+  const size_t units = (bytes + 15) / 16;
+  int blocks = c->blocks > 0 ? c->blocks
+                             : static_cast<int>(std::min<size_t>(c->max_ctas,
+                                                                 (units + c->threads - 1) / c->threads));
+  blocks = std::max(1, std::min({blocks, c->max_ctas, kSeqSlots}));
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks, 1);
+  cfg.blockDim = dim3(c->threads);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 0;
+  if (c->pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 1;
+  }
+  CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k, lp));
+  return NVRAR_SUCCESS;
 }
 
 int nvrar_allreduce_residual(nvrar_comm_t comm, const void* send, void* recv,

@@ -28,6 +28,7 @@
 namespace nvrar {
 
 constexpr int kMaxRanks = 64;   // NVRAR_MAX_RANKS
+constexpr int kCtrlWords = 3 * kMaxRanks;  // counters, diag (+pad), done
 constexpr int kMaxLocal = 32;   // NVRAR_MAX_LOCAL (virtual ranks per launch)
 constexpr int kThreads = 512;   // threads per CTA
 constexpr int kDirectThreads = 256;  // direct schedule (no waits; several CTAs per SM)
@@ -45,7 +46,8 @@ enum WaitKind : int32_t { kFlagWait = 0, kSeqWait = 1, kLenMismatch = 2, kStaleF
 
 // Byte offsets inside the symmetric region; identical on every rank.
 struct Layout {
-  uint64_t ctrl_off;  // u64 counters[kMaxRanks]: counters[p] = (seq<<32)|len from rank p
+  uint64_t ctrl_off;  // control words, kCtrlWords u64: counters[kMaxRanks] ((seq<<32)|len
+                      // from rank p), the ping-pong diag word, done[kMaxRanks]
   uint64_t a_off;     // A slots: [2 parity][P src][a_src words]  (RS / one-shot inputs)
   uint64_t a_src;     // words (8 B) per source slot
   uint64_t b_off;     // B slots: [2][P][b_src]                    (all-gather)
@@ -79,6 +81,7 @@ constexpr int kPhases = 8;
 struct RankState {
   uint32_t seq[kSeqSlots];
   ErrRec err;
+  uint32_t arrive;  // CTAs of the current registered-buffer launch that finished reading
   uint64_t ts[kSeqSlots][kPhases];  // per-CTA phase timestamps, thread 0 (profiling)
 };
 
@@ -681,6 +684,11 @@ __device__ __forceinline__ uint64_t* counters(const RankDesc& d, int rank) {
 // ping-pong word (signal-latency probe), right after the counters
 __device__ __forceinline__ uint64_t* diag_word(const RankDesc& d, int rank) {
   return counters(d, rank) + kMaxRanks;
+}
+// done[p] = (seq<<32)|len from rank p: p finished reading this rank's
+// registered buffer for call seq (nvrar_allreduce_registered)
+__device__ __forceinline__ uint64_t* done_words(const RankDesc& d, int rank) {
+  return counters(d, rank) + 2 * kMaxRanks;
 }
 
 // Programmatic dependent launch: everything before pdl_wait() may overlap the

@@ -927,6 +927,169 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
 
 using KernelFn = void (*)(LaunchParams);
 
+// ---------------------------------------------------------------------------
+// Registered-buffer one-shot (nvrar_allreduce_registered): every rank's INPUT
+// lives in a buffer registered with the comm and mapped into every peer
+// (Ctx::alloc_region's symmetric regions, transport.hpp:146-148), so nothing
+// is staged: each rank announces that its input is final (the seq/len word),
+// reads every peer's input in place over NVLink, folds each unit in the
+// reference order (as direct_kernel) and writes its own output. Its input may
+// be overwritten by the caller once this launch completes, so the launch does
+// not complete before every peer has finished reading it: the last CTA to
+// finish reading posts done(seq) to each peer and waits for theirs.
+// lp.send[r] = rank r's input as mapped here (r = global rank, P <= 32).
+template <class E, int N, int MAXG>
+__global__ void __launch_bounds__(kThreads, 1) pull_kernel(const __grid_constant__ LaunchParams lp) {
+  using A = typename E::acc;
+  constexpr int UE = 16 / E::kBytes;
+  constexpr int RDW = 4;
+  constexpr int kLevels = Log2<N>::value + 1;
+  const RankDesc& d = lp.d0;
+  begin_wait(d);
+  Ctl c;
+  if (!begin_seq(d, c)) return;
+  const int P = d.world, me = d.rank, G = d.gpus;
+  const uint32_t n = static_cast<uint32_t>(lp.count);
+  const uint32_t SG = (n + G - 1) / G;
+  const uint32_t U = (n + UE - 1) / UE;
+  const uint32_t ub = static_cast<uint32_t>(static_cast<uint64_t>(U) * blockIdx.x / gridDim.x);
+  const uint32_t ue = static_cast<uint32_t>(static_cast<uint64_t>(U) * (blockIdx.x + 1) / gridDim.x);
+  // ready: our input is final (stream order), peers may read it
+  if (blockIdx.x == 0) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      if (p != me) publish_seq_len(d, p, c.seq, n);
+    }
+  }
+  c.phase = 3;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    if (p != me) wait_seq_len(c, d, p, n);
+  }
+  __syncthreads();  // also a compiler barrier: no input load moves above the wait
+  c.phase = 4;
+  for (uint32_t u = ub + threadIdx.x; u < ue && !c.aborted; u += blockDim.x) {
+    const uint32_t e0 = UE * u;
+    const int valid = clamp_valid<UE>(static_cast<int64_t>(n) - static_cast<int64_t>(e0));
+    const int c0 = static_cast<int>(e0 / SG);
+    const bool straddle = e0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG;
+    int l0 = c0 + 1;
+    if (l0 >= G) l0 -= G;
+    uint32_t r[N][MAXG][RDW];
+#pragma unroll
+    for (int nn = 0; nn < N; ++nn) {
+      int l = l0;
+#pragma unroll
+      for (int j = 0; j < MAXG; ++j) {
+        if (j < G) {
+          load_raw<E, UE>(lp.send[nn * G + l], e0, valid, r[nn][j]);
+          l = l + 1 == G ? 0 : l + 1;
+        }
+      }
+    }
+    A stack[kLevels][UE];
+#pragma unroll
+    for (int nn = 0; nn < N; ++nn) {
+      A v[UE];
+      if (!straddle) {
+        raw_to_acc<UE>(E{}, r[nn][0], v);
+#pragma unroll
+        for (int j = 1; j < MAXG; ++j) {
+          if (j < G) {
+            A a[UE];
+            raw_to_acc<UE>(E{}, r[nn][j], a);
+#pragma unroll
+            for (int q = 0; q < UE; ++q) v[q] = acc_add(v[q], a[q]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < UE; ++q) {
+          const int cq = q < valid ? static_cast<int>((e0 + q) / SG) : c0;
+          const int rot = cq - c0;
+          A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % G, q);
+#pragma unroll
+          for (int j = 1; j < MAXG; ++j) {
+            if (j < G) x = acc_add(x, pick<E, UE, RDW, N, MAXG>(r, nn, (j + rot) % G, q));
+          }
+          v[q] = x;
+        }
+      }
+      int lvl = 0;
+#pragma unroll
+      for (int k = 0; k < kLevels - 1; ++k) {
+        if (((nn >> k) & 1) && lvl == k) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) v[q] = acc_add(stack[k][q], v[q]);
+          lvl = k + 1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kLevels; ++k) {
+        if (k == lvl) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) stack[k][q] = v[q];
+        }
+      }
+    }
+    uint32_t o[RDW];
+    acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
+    emit<E, UE>(lp.recv[0], lp.resid[0], e0, valid, o);
+  }
+  // every thread's loads have returned (their values were stored): count this CTA
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    s_last = atomicAdd(&d.state->arrive, 1u) == gridDim.x - 1u;
+    if (s_last) d.state->arrive = 0u;  // the next call's CTAs start after this grid
+  }
+  __syncthreads();
+  c.phase = 5;
+  if (s_last) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      if (p != me) {
+        st_volatile64(done_words(d, p) + me, (static_cast<uint64_t>(c.seq) << 32) | n);
+      }
+    }
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      if (p == me) continue;
+      const uint64_t* w = done_words(d, me) + p;
+      while (true) {
+        const uint64_t v = ld_volatile64(w);
+        const uint32_t s = static_cast<uint32_t>(v >> 32);
+        if (s == c.seq || flag_ahead(s, c.seq)) break;
+        if (wait_tick(c, kSeqWait, p, 0, v)) break;
+        poll_pause(c);
+      }
+    }
+  }
+  end_call(d, c.seq);
+}
+
+template <class E>
+KernelFn pull_for(int nodes, int gpus) {
+  KernelFn k = nullptr;
+  switch (nodes) {
+    case 1:
+      k = gpus <= 1 ? pull_kernel<E, 1, 1> : gpus <= 2 ? pull_kernel<E, 1, 2>
+        : gpus <= 4 ? pull_kernel<E, 1, 4> : gpus <= 8 ? pull_kernel<E, 1, 8> : nullptr;
+      break;
+    case 2:
+      k = gpus <= 1 ? pull_kernel<E, 2, 1> : gpus <= 2 ? pull_kernel<E, 2, 2>
+        : gpus <= 4 ? pull_kernel<E, 2, 4> : gpus <= 8 ? pull_kernel<E, 2, 8> : nullptr;
+      break;
+    case 4:
+      k = gpus <= 1 ? pull_kernel<E, 4, 1> : gpus <= 2 ? pull_kernel<E, 4, 2>
+        : gpus <= 4 ? pull_kernel<E, 4, 4> : gpus <= 8 ? pull_kernel<E, 4, 8> : nullptr;
+      break;
+    case 8:
+      k = gpus <= 1 ? pull_kernel<E, 8, 1> : gpus <= 2 ? pull_kernel<E, 8, 2>
+        : gpus <= 4 ? pull_kernel<E, 8, 4> : nullptr;
+      break;
+    default:
+      break;
+  }
+  return k;
+}
+
 // MAXG = pow2 >= gpus per node (the per-thread source tile r[N][MAXG]), N * MAXG <= 32.
 template <class E, int N>
 KernelFn direct_for_n(int gpus) {
@@ -1031,5 +1194,8 @@ KernelFn kernel_direct_i32(int nodes, int gpus);
 KernelFn kernel_phase_f32(int mode, int nodes, bool emu);
 KernelFn kernel_phase_bf16(int mode, int nodes, bool emu);
 KernelFn kernel_phase_i32(int mode, int nodes, bool emu);
+KernelFn kernel_pull_f32(int nodes, int gpus);
+KernelFn kernel_pull_bf16(int nodes, int gpus);
+KernelFn kernel_pull_i32(int nodes, int gpus);
 
 }  // namespace nvrar

@@ -76,6 +76,15 @@ KernelFn select_phase(int dtype, int mode, int nodes, bool emu) {
   }
 }
 
+KernelFn select_pull(int dtype, int nodes, int gpus) {
+  switch (dtype) {
+    case 0: return kernel_pull_i32(nodes, gpus);
+    case 1: return kernel_pull_f32(nodes, gpus);
+    case 2: return kernel_pull_bf16(nodes, gpus);
+    default: return nullptr;
+  }
+}
+
 KernelFn bump_kernel() { return seq_bump_kernel; }
 
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);

@@ -173,6 +173,50 @@ def host_mixed(comm, rank, nodes, gpus, log):
     return fails
 
 
+def registered(comm, rank, nodes, gpus, device, log):
+    """nvrar_allreduce_registered: inputs in a buffer registered with the comm,
+    read in place by the peers. Each call's input is overwritten right after
+    the call (stream order) with the next call's — correct only if no launch
+    completes before every peer has read its input — and registered calls
+    interleave with staged ones on the same call sequence."""
+    world = nodes * gpus
+    fails = 0
+    cap = 70000
+    bufs = {dt: comm.alloc_symmetric(cap, dt) for dt in (torch.float32, torch.bfloat16,
+                                                         torch.int32)}
+    names = {torch.float32: "f32", torch.bfloat16: "bf16", torch.int32: "i32"}
+    for dt, buf in bufs.items():
+        dtype = names[dt]
+        outs, wants = [], []
+        for k, n in enumerate((1, 4099, 65539, 65539)):
+            x = _inputs(dtype, world, n, 630 + k)
+            src = _dev(x[rank], dtype, device)
+            off = 8 * k  # a different offset each call, the same on every rank
+            buf[off:off + n].copy_(src)
+            out = torch.empty_like(src)
+            comm.allreduce_registered(buf[off:off + n], out)
+            buf[off:off + n].fill_(0)  # overwrite at once: must not reach any peer
+            if k == 2:
+                extra = torch.empty_like(src)
+                comm.allreduce(src, extra)  # a staged call in between
+                outs.append(extra)
+                wants.append(_want(x, nodes, gpus, dtype))
+            outs.append(out)
+            wants.append(_want(x, nodes, gpus, dtype))
+        torch.cuda.synchronize(device)
+        comm.check()
+        for i, (o, w) in enumerate(zip(outs, wants)):
+            if not np.array_equal(_host(o, dtype), w):
+                fails += 1
+                log(f"registered all-reduce {dtype} call {i} differs")
+    # a peer's registered range is reachable through its mapping here
+    peer = (rank + 1) % world
+    if world > 1 and comm.buffer_peer_ptr(1, peer) == 0:
+        fails += 1
+        log("no peer mapping for registered buffer 1")
+    return fails
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dir", required=True)
@@ -183,6 +227,8 @@ def main():
     ap.add_argument("--quick", action="store_true", help="fewer sizes and dtypes")
     ap.add_argument("--ops", action="store_true", help="also the torch.ops.nvrar entry points")
     ap.add_argument("--mismatch", action="store_true", help="length-mismatch protocol fault")
+    ap.add_argument("--registered", action="store_true",
+                    help="all-reduce of registered (symmetric) buffers read in place")
     ap.add_argument("--host", action="store_true",
                     help="host-buffer path, pinned on even ranks and pageable on odd ranks")
     ap.add_argument("--timeout", type=float, default=60.0)
@@ -214,6 +260,8 @@ def main():
     dtypes = ("f32", "bf16") if args.quick else ("f32", "bf16", "i32")
     sizes = (4099,) if args.quick else (1, 4099, 65539)
     fails = parity(comm, rank, args.nodes, args.gpus, device, algos, dtypes, sizes, log)
+    if args.registered:
+        fails += registered(comm, rank, args.nodes, args.gpus, device, log)
     if args.host:
         fails += host_mixed(comm, rank, args.nodes, args.gpus, log)
     if args.ops:

@@ -92,3 +92,13 @@ def test_timesliced_host_path_mixed_memory(nodes, gpus):
     rcs, out = run_ranks(nodes, gpus, ("--quick", "--host"))
     assert all(rc == 0 for rc in rcs), out[-4000:]
     assert out.count(": OK") == nodes * gpus, out[-4000:]
+
+
+@pytest.mark.parametrize("nodes,gpus", [(2, 1), (1, 2), (2, 2), (4, 1)])
+def test_timesliced_registered_buffers(nodes, gpus):
+    """nvrar_register_buffer / nvrar_connect_buffer (Ctx::alloc_region,
+    transport.hpp:146-148) and the in-place all-reduce of registered inputs,
+    interleaved with staged calls, bit-exact against the oracle."""
+    rcs, out = run_ranks(nodes, gpus, ("--quick", "--registered"))
+    assert all(rc == 0 for rc in rcs), out[-4000:]
+    assert out.count(": OK") == nodes * gpus, out[-4000:]
