@@ -371,6 +371,22 @@ int nvrar_debug_dirty_cells(nvrar_comm_t comm, uint64_t* dirty, uint64_t* first_
  * b_src, c_off, c_step, bytes). Synchronises. */
 int nvrar_debug_read_region(nvrar_comm_t comm, uint64_t offset, uint64_t bytes, void* host,
                             uint64_t* layout);
+/* Delay injection (tests; the reference's RunOptions::delay_max_us,
+ * concurrent_transport.hpp:393-419, acceptance_test.cpp:314-330): every warp
+ * sleeps a seeded pseudo-random 0..max_ns ns before its remote stores and
+ * between unsatisfied polls, so adversarial interleavings are exercised. The
+ * results must not change. max_ns = 0 turns it off; at most 1 ms. */
+int nvrar_set_jitter(nvrar_comm_t comm, uint32_t max_ns, uint32_t seed);
+/* Word-atomicity canary (acceptance_test.cpp:338-364): the writer (writer = 1)
+ * streams `iters` 16-byte fused cells into `peer`'s canary cell, the reader
+ * (the peer, writer = 0, launched first or concurrently) checks every cell it
+ * observes for tearing. Asynchronous on `stream` (the two sides may be comms
+ * of one process on two streams); nvrar_debug_canary_result synchronises and
+ * gives the torn observations (reader) or 0 (writer). Both sides call it the
+ * same number of times per pair. */
+int nvrar_debug_canary(nvrar_comm_t comm, int peer, int iters, int writer, uint32_t jitter_ns,
+                       uint32_t seed, void* stream);
+int nvrar_debug_canary_result(nvrar_comm_t comm, uint32_t* torn);
 /* Debug: the per-CTA replicas of the call counter (all equal between calls). */
 int nvrar_debug_seq_slots(nvrar_comm_t comm, uint32_t* out, int n);
 const char* nvrar_last_error(nvrar_comm_t comm);

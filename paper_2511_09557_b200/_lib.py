@@ -143,6 +143,10 @@ SIGNATURES = {
     "nvrar_debug_read_region": (_c.c_int, [_vp, _c.c_uint64, _c.c_uint64, _vp,
                                            _c.POINTER(_c.c_uint64)]),
     "nvrar_debug_seq_slots": (_c.c_int, [_vp, _c.POINTER(_c.c_uint32), _c.c_int]),
+    "nvrar_set_jitter": (_c.c_int, [_vp, _c.c_uint32, _c.c_uint32]),
+    "nvrar_debug_canary": (_c.c_int, [_vp, _c.c_int, _c.c_int, _c.c_int, _c.c_uint32,
+                                      _c.c_uint32, _vp]),
+    "nvrar_debug_canary_result": (_c.c_int, [_vp, _c.POINTER(_c.c_uint32)]),
     "nvrar_check":(_c.c_int, [_vp]),
     "nvrar_get_blocked": (_c.c_int, [_vp, _c.POINTER(Blocked)]),
     "nvrar_last_error": (_c.c_char_p, [_vp]),

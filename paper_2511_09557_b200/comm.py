@@ -348,6 +348,22 @@ class Communicator:
         """'auto' | 'll' (fused seq words, as the reference) | 'lamport' (raw payload)."""
         self._check(self._lib.nvrar_set_protocol(self._h, L.PROTO_CODES[proto]))
 
+    def set_jitter(self, max_ns: int, seed: int = 0) -> None:
+        """Delay injection (RunOptions::delay_max_us analogue): seeded random
+        sleeps of up to max_ns before remote stores and between polls; 0 = off."""
+        self._check(self._lib.nvrar_set_jitter(self._h, max_ns, seed & 0xFFFFFFFF))
+
+    def canary(self, peer: int, iters: int, writer: bool, jitter_ns: int = 0, seed: int = 0,
+               stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Launch one side of the word-atomicity canary (nvrar_debug_canary)."""
+        self._check(self._lib.nvrar_debug_canary(self._h, peer, iters, int(writer), jitter_ns,
+                                                 seed & 0xFFFFFFFF, _stream_ptr(stream)))
+
+    def canary_result(self) -> int:
+        t = ctypes.c_uint32()
+        self._check(self._lib.nvrar_debug_canary_result(self._h, ctypes.byref(t)))
+        return t.value
+
     def plan(self, count: int, dtype: torch.dtype):
         a, b = ctypes.c_int(), ctypes.c_int()
         self._check(self._lib.nvrar_plan(self._h, count, dtype_code(dtype), ctypes.byref(a),
@@ -639,6 +655,10 @@ class LocalGroup:
     def set_protocol(self, proto: str) -> None:
         for c in self.comms:
             c.set_protocol(proto)
+
+    def set_jitter(self, max_ns: int, seed: int = 0) -> None:
+        for r, c in enumerate(self.comms):
+            c.set_jitter(max_ns, seed * 131 + r)
 
     def set_host_chunk(self, nbytes: int) -> None:
         for c in self.comms:

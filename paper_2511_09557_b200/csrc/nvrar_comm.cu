@@ -25,6 +25,8 @@ KernelFn select_phase(int dtype, int mode, int nodes, bool emu);
 KernelFn select_pull(int dtype, int nodes, int gpus);
 using PingFn = void (*)(LaunchParams, int, int, uint64_t, int, uint64_t*);
 PingFn pingpong_fn();
+using CanaryFn = void (*)(LaunchParams, int, int, int, uint32_t, uint32_t, uint32_t, uint32_t*);
+CanaryFn canary_fn();
 int flat_max_gpus(int nodes);
 }  // namespace nvrar
 
@@ -101,6 +103,7 @@ struct nvrar_comm {
   int proto = NVRAR_PROTO_AUTO;
   int threads = kThreads;  // threads per CTA (multiple of 32, <= kThreads)
   uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
+  uint32_t canary_base[kMaxRanks] = {};  // per-peer canary flag base (same on both sides)
   uint64_t* d_scratch = nullptr;
   std::vector<nvrar_plan_entry> table;  // measured selector (ascending max_bytes)
   bool mc_ready = false;  // NVLS multicast area attached (nvrar_mc_attach)
@@ -1239,6 +1242,47 @@ int nvrar_pingpong(nvrar_comm_t c, int peer, int iters, int initiator, void* str
   CUDA_TRY(c, cudaStreamSynchronize(s));
   CUDA_TRY(c, cudaMemcpy(elapsed_ns, c->d_scratch, sizeof(uint64_t), cudaMemcpyDeviceToHost));
   if (*elapsed_ns == ~0ull) return fail(c, NVRAR_ERR_DEADLOCK, "pingpong timed out");
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_set_jitter(nvrar_comm_t c, uint32_t max_ns, uint32_t seed) {
+  if (!c) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null comm");
+  if (max_ns > 1000000u) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "jitter above 1 ms");
+  c->h_desc.jitter_ns = max_ns;
+  c->h_desc.jitter_seed = seed;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpy(c->d_desc, &c->h_desc, sizeof(RankDesc), cudaMemcpyHostToDevice));
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_debug_canary(nvrar_comm_t c, int peer, int iters, int writer, uint32_t jitter_ns,
+                       uint32_t seed, void* stream) {
+  if (!c || peer < 0 || peer >= c->world || peer == c->rank || iters < 1 ||
+      iters > (1 << 20)) {
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "bad canary argument");
+  }
+  if (!c->connected) return fail(c, NVRAR_ERR_NOT_CONNECTED, "comm not connected");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  LaunchParams lp{};
+  lp.d0 = c->h_desc;
+  lp.nlocal = 1;
+  // flags unique per (pair, run): a previous run's cell never matches this run's last flag
+  const uint32_t base = c->canary_base[peer] + 1u;
+  c->canary_base[peer] += static_cast<uint32_t>(iters) + 1u;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* out = reinterpret_cast<uint32_t*>(c->d_scratch) + 8;  // scratch words 4..
+  canary_fn()<<<1, 32, 0, s>>>(lp, peer, iters, writer, base, jitter_ns, seed, out);
+  CUDA_TRY(c, cudaGetLastError());
+  return NVRAR_SUCCESS;
+}
+
+int nvrar_debug_canary_result(nvrar_comm_t c, uint32_t* torn) {
+  if (!c || !torn) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  CUDA_TRY(c, cudaMemcpy(torn, reinterpret_cast<uint32_t*>(c->d_scratch) + 8, sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost));
+  if (*torn == ~0u) return fail(c, NVRAR_ERR_DEADLOCK, "canary reader timed out");
   return NVRAR_SUCCESS;
 }
 

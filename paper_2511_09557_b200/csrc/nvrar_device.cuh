@@ -99,6 +99,12 @@ struct RankDesc {
   // multicast is not set up.
   uint8_t* mc;
   uint8_t* mc_local;
+  // Delay injection (nvrar_set_jitter; the GPU counterpart of the reference's
+  // RunOptions::delay_max_us, concurrent_transport.hpp:393-419): when
+  // jitter_ns > 0 every CTA warp sleeps a seeded pseudo-random 0..jitter_ns ns
+  // before its remote stores and between unsatisfied polls. 0 = off.
+  uint32_t jitter_ns;
+  uint32_t jitter_seed;
 };
 
 // One rank per launch (the real multi-GPU path) passes its descriptor BY VALUE
@@ -203,6 +209,7 @@ struct Ctl {
   RankState* st;
   uint64_t timeout_ns;
   uint32_t poll_ns;
+  uint32_t jitter_ns, jitter_seed;
   uint32_t seq;
   uint32_t spins;
   uint64_t t0;
@@ -256,8 +263,31 @@ __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t w
 // lets the other diverged lane groups of the warp run: a tight spin without it
 // was observed to starve lanes whose data had already arrived (independent
 // thread scheduling does not rotate diverged groups often enough).
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
 __device__ __forceinline__ void poll_pause(const Ctl& c) {
   __nanosleep(c.poll_ns ? c.poll_ns : 32u);
+  if (c.jitter_ns) {
+    __nanosleep(mix32(c.jitter_seed ^ mix32(c.spins * 0x9E3779B9u ^ threadIdx.x ^
+                                            (blockIdx.x << 16))) % c.jitter_ns);
+  }
+}
+
+// Injected delay at a program point (`site`) of call `seq`: the same for a
+// whole warp (per CTA, warp, unit group and site), different per seed.
+__device__ __forceinline__ void jitter(const Ctl& c, uint32_t site) {
+  if (c.jitter_ns == 0) return;
+  const uint32_t h = mix32(c.jitter_seed ^ mix32(c.seq * 0x9E3779B9u ^ (blockIdx.x << 20) ^
+                                                 (blockIdx.y << 26) ^ ((threadIdx.x >> 5) << 8) ^
+                                                 site));
+  __nanosleep(h % c.jitter_ns);
 }
 
 // flag observed in a slot for call `seq`: equal = arrived; behind = not yet
@@ -684,6 +714,10 @@ __device__ __forceinline__ uint64_t* counters(const RankDesc& d, int rank) {
 // ping-pong word (signal-latency probe), right after the counters
 __device__ __forceinline__ uint64_t* diag_word(const RankDesc& d, int rank) {
   return counters(d, rank) + kMaxRanks;
+}
+// 16-byte cell of the word-atomicity canary (nvrar_debug_canary), in the diag block
+__device__ __forceinline__ uint4* canary_cell(const RankDesc& d, int rank) {
+  return reinterpret_cast<uint4*>(counters(d, rank) + kMaxRanks + 2);
 }
 // done[p] = (seq<<32)|len from rank p: p finished reading this rank's
 // registered buffer for call seq (nvrar_allreduce_registered)

@@ -112,6 +112,8 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, SeqWords w)
   c.st = d.state;
   c.timeout_ns = d.timeout_ns;
   c.poll_ns = d.poll_ns;
+  c.jitter_ns = d.jitter_ns;
+  c.jitter_seed = d.jitter_seed;
   c.spins = 0;
   c.aborted = false;
   c.last_chance = false;
@@ -259,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   }
 
   // Phase 1a: reduce-scatter pushes (ring_reduce_scatter_phase, ring_schedule.hpp:33-58).
+  jitter(c, 1);
   if (kFold && G > 1) {
 #pragma unroll
     for (int j = 1; j < MG; ++j) {
@@ -379,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     for (int l = 0; l < kSteps; ++l) {
       const int partner = ((node ^ (1 << l)) * G) + local;
       uint4* dst = slot_c(d, partner, parity, l);
+      jitter(c, 16 + l + static_cast<uint32_t>(u0 >> 5) * 64);
 #pragma unroll
       for (int k = 0; k < kHierUpt; ++k) {
         if (valid[k] == 0) continue;
@@ -414,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
 
     // Final cast, own output, all-gather push (ring_all_gather_phase, ring_schedule.hpp:62-83).
+    jitter(c, 3 + static_cast<uint32_t>(u0 >> 5) * 64);
 #pragma unroll
     for (int k = 0; k < kHierUpt; ++k) {
       if constexpr (kRS) {
@@ -574,6 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
   }
 
+  jitter(c, 1);
   // Reduce-scatter pushes: the owner q of each sub-shard receives our copy.
   // Multicast one-shot: ONE store per cell to the multicast mapping reaches
   // slot `me` of every rank's multicast A area (the NVSwitch replicates it).
@@ -750,6 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
     emit<E, UE>(recv, resid, e0, valid, o);
     if (!oneshot) {
+      jitter(c, 3 + static_cast<uint32_t>(u >> 5) * 64);
       int q = me;
       for (int j = 1; j < P; ++j) {
         q = q + 1 == P ? 0 : q + 1;
@@ -955,6 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1) pull_kernel(const __grid_constant
   const uint32_t ub = static_cast<uint32_t>(static_cast<uint64_t>(U) * blockIdx.x / gridDim.x);
   const uint32_t ue = static_cast<uint32_t>(static_cast<uint64_t>(U) * (blockIdx.x + 1) / gridDim.x);
   // ready: our input is final (stream order), peers may read it
+  jitter(c, 1);
   if (blockIdx.x == 0) {
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       if (p != me) publish_seq_len(d, p, c.seq, n);
@@ -1043,6 +1051,7 @@ __global__ void __launch_bounds__(kThreads, 1) pull_kernel(const __grid_constant
   }
   __syncthreads();
   c.phase = 5;
+  jitter(c, 5);
   if (s_last) {
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       if (p != me) {

@@ -49,6 +49,49 @@ __global__ void pingpong_kernel(const __grid_constant__ LaunchParams lp, int pee
   out_ns[2] = t_last_recv;
 }
 
+// Word-atomicity canary (acceptance_test.cpp:338-364, criterion 7, on the GPU
+// transport): the writer streams 16-byte fused cells {i*K, base+i, i*K, base+i}
+// into the peer's canary cell with seeded delays between stores; the reader
+// polls its own cell and checks every observation: both flags equal and each
+// data word the function of its flag. A torn cell (a mix of two stores) breaks
+// the relation. out[0] = torn observations (reader) / 0 (writer), ~0 = timeout.
+__global__ void canary_kernel(const __grid_constant__ LaunchParams lp, int peer, int iters,
+                              int writer, uint32_t base, uint32_t jitter_ns, uint32_t seed,
+                              uint32_t* out) {
+  const RankDesc& d = lp.d0;
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  constexpr uint32_t K = 2654435761u;
+  const uint64_t t_limit = globaltimer() + d.timeout_ns;
+  if (writer) {
+    uint4* theirs = canary_cell(d, peer);
+    for (int i = 1; i <= iters; ++i) {
+      const uint32_t f = base + static_cast<uint32_t>(i);
+      st_volatile16(theirs, f * K, f, f * K, f);
+      if (jitter_ns) __nanosleep(mix32(seed ^ mix32(static_cast<uint32_t>(i))) % jitter_ns);
+    }
+    out[0] = 0;
+    return;
+  }
+  const uint4* mine = canary_cell(d, d.rank);
+  uint32_t torn = 0;
+  const uint32_t last = base + static_cast<uint32_t>(iters);
+  for (uint32_t spins = 0;; ++spins) {
+    const uint4 v = ld_volatile16(mine);
+    const bool empty = (v.x & v.y & v.z & v.w) == 0xFFFFFFFFu;
+    if (!empty && (v.y != v.w || v.x != v.y * K || v.z != v.w * K)) ++torn;
+    if (v.y == last && v.w == last) break;
+    if (jitter_ns) __nanosleep(mix32(seed ^ spins) % jitter_ns);
+    if ((spins & 255u) == 0u && globaltimer() > t_limit) {
+      out[0] = ~0u;
+      return;
+    }
+  }
+  out[0] = torn;
+}
+
+using CanaryFn = void (*)(LaunchParams, int, int, int, uint32_t, uint32_t, uint32_t, uint32_t*);
+CanaryFn canary_fn() { return canary_kernel; }
+
 KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport) {
   switch (dtype) {
     case 0: return flat ? kernel_flat_i32(nodes, gpus, emu, false) : kernel_hier_i32(nodes, gpus, emu, false);

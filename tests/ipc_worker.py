@@ -232,6 +232,10 @@ def main():
     ap.add_argument("--host", action="store_true",
                     help="host-buffer path, pinned on even ranks and pageable on odd ranks")
     ap.add_argument("--timeout", type=float, default=60.0)
+    ap.add_argument("--jitter-seeds", type=int, default=0,
+                    help="repeat the parity grid under delay injection with this many seeds")
+    ap.add_argument("--canary", type=int, default=0,
+                    help="word-atomicity canary runs between ranks 0 (writer) and 1 (reader)")
     args = ap.parse_args()
     rank = args.rank
     world = args.nodes * args.gpus
@@ -260,6 +264,18 @@ def main():
     dtypes = ("f32", "bf16") if args.quick else ("f32", "bf16", "i32")
     sizes = (4099,) if args.quick else (1, 4099, 65539)
     fails = parity(comm, rank, args.nodes, args.gpus, device, algos, dtypes, sizes, log)
+    for seed in range(args.jitter_seeds):
+        comm.set_jitter(3000, seed * 7919 + rank)
+        fails += parity(comm, rank, args.nodes, args.gpus, device, algos, dtypes, (4099 + seed,),
+                        lambda m, s=seed: log(f"jitter seed {s}: {m}"))
+        comm.set_jitter(0)
+    for seed in range(args.canary):
+        if rank in (0, 1) and world > 1:
+            comm.canary(1 - rank, 64, writer=rank == 0, jitter_ns=1000, seed=seed)
+            torn = comm.canary_result()
+            if torn:
+                fails += 1
+                log(f"canary seed {seed}: {torn} torn cells")
     if args.registered:
         fails += registered(comm, rank, args.nodes, args.gpus, device, log)
     if args.host:

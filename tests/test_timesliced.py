@@ -102,3 +102,14 @@ def test_timesliced_registered_buffers(nodes, gpus):
     rcs, out = run_ranks(nodes, gpus, ("--quick", "--registered"))
     assert all(rc == 0 for rc in rcs), out[-4000:]
     assert out.count(": OK") == nodes * gpus, out[-4000:]
+
+
+@pytest.mark.parametrize("nodes,gpus", [(2, 1), (2, 2)])
+def test_timesliced_delay_injection(nodes, gpus):
+    """Criterion 7 across processes: the parity grid under 8 seeds of injected
+    delays (up to 3 us before remote stores and between polls), results
+    bit-exact; plus 20 rounds of the word-atomicity canary between two
+    processes."""
+    rcs, out = run_ranks(nodes, gpus, ("--quick", "--jitter-seeds", "8", "--canary", "20"))
+    assert all(rc == 0 for rc in rcs), out[-4000:]
+    assert out.count(": OK") == nodes * gpus, out[-4000:]
