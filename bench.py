@@ -36,6 +36,42 @@ METRIC = "all-reduce p50 latency (µs, max over ranks) 128KB–2MB at 2/4/8 B200
 NVLINK_PEAK_GBS = 770.0     # measured B200 peer copy per direction (B200_PROFILING.md)
 NVLINK_NOMINAL_GBS = 900.0  # NVLink 5 per direction per GPU
 SWEEP = [64 << 10, 128 << 10, 256 << 10, 512 << 10, 1 << 20, 2 << 20, 4 << 20, 8 << 20]
+PRODUCER_SIZES = (128 << 10, 512 << 10, 1 << 20, 2 << 20)
+
+
+def nccl_best_table(world):
+    """Per message size, the best NCCL (algorithm x protocol x library) measured on
+    this pool by `rankbench nccl-best` (profiles/*nccl_best_p{world}*.jsonl)."""
+    import glob
+    out = {}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*nccl_best_p{world}*.jsonl")),
+                       reverse=True):
+        with open(path) as fh:
+            for line in fh:
+                if line.startswith("BEST "):
+                    r = json.loads(line[5:])
+                    if r.get("producer", "none") == "none":
+                        out.setdefault(int(r["bytes"]), r)
+        return out, os.path.basename(path)
+    return out, None
+
+
+def profiled_nvlink_traffic(world, algo, msg):
+    """NVLink bytes (TX + RX) per launch of the schedule's kernel at this size and
+    world, from the committed single-pass ncu capture of rank 0
+    (profiles/*ncu_nvlink*.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_nvlink*.json")),
+                       reverse=True):
+        try:
+            with open(path) as fh:
+                p = json.load(fh)
+            for r in p["rows"]:
+                if r["world"] == world and r["algo"] == algo and r["bytes"] == msg:
+                    return int(r["nvl_tx_bytes"] + r["nvl_rx_bytes"]), os.path.basename(path)
+        except Exception:
+            continue
+    return None, None
 
 
 def profiled_traffic(kernel_prefix):
@@ -288,7 +324,21 @@ def run_multi(args, rank, world, local):
     if not args.no_autotune:
         tuned = S.autotune(comm, sizes=SWEEP, dtype=torch.bfloat16, calls=30, reps=5)
 
-    def measure(msg, impl, steps, warmup):
+    # ncclAllReduce called directly (torch's libnccl, default algorithm and
+    # protocol), captured in the same graphs as NVRAR; torch.distributed's
+    # all_reduce is kept as the framework-level reference
+    from paper_2511_09557_b200 import nccl_ref
+    ncc = nccl_ref.Nccl(nccl_ref.lib_path("torch"))
+    uid = [ncc.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    ncc.init_rank(world, uid[0], rank)
+    nccl_version = ncc.version()
+
+    def measure(msg, impl, steps, warmup, producer=False):
+        """p50-sorted per-call µs (max over ranks). producer: a cuBLAS GEMM writes
+        each call's input first (the decode layer's projection): no PDL chaining
+        to the previous all-reduce, L2-hot input; the per-call all-reduce cost is
+        (step - GEMM-only step) / calls, the same subtraction for every arm."""
         ne = msg // 2
         calls = H.calls_for(msg, 1)
         torch.manual_seed(1234 + rank)
@@ -297,26 +347,48 @@ def run_multi(args, rank, world, local):
         if impl == "nvrar":
             plan = D.plan_consensus(comm.plan(ne, torch.bfloat16))
             fn = lambda i: comm.allreduce(bufs[i][0], bufs[i][1])  # noqa: E731
+        elif impl == "nccl":
+            plan = ("nccl-direct", 0)
+            fn = lambda i: ncc.all_reduce(bufs[i][0], bufs[i][1])  # noqa: E731
         else:
-            plan = ("nccl", 0)
+            plan = ("torch.distributed", 0)
             fn = lambda i: dist.all_reduce(bufs[i][1])  # noqa: E731
             for a, b in bufs:
                 b.copy_(a)
+        base = 0.0
+        if producer:
+            rows, k = max(1, ne // 8192), 1024
+            xs = [torch.randn(rows, k, device="cuda").to(torch.bfloat16) for _ in range(4)]
+            w = (torch.randn(k, ne // rows, device="cuda") * k ** -0.5).to(torch.bfloat16)
+            dst = 1 if impl == "torch" else 0
+
+            def prod(i):
+                torch.matmul(xs[i % 4], w, out=bufs[i][dst].view(rows, ne // rows))
+            g0 = H.graph_of(prod, calls, stream)
+            t0 = D.max_over_ranks(H.time_replays(g0.replay, steps, warmup, barrier, stream),
+                                  device=dev)
+            base = statistics.median(t0)
+            del g0
+            inner = fn
+            fn = lambda i: (prod(i), inner(i))  # noqa: E731
         gr = H.graph_of(fn, calls, stream)
         ts = H.time_replays(gr.replay, steps, warmup, barrier, stream)
         ts = D.max_over_ranks(ts, device=dev)
         if impl == "nvrar":
             comm.check()
         del gr
-        return sorted(t * 1e3 / calls for t in ts), calls, plan
+        return sorted((t - base) * 1e3 / calls for t in ts), calls, plan
 
     hbm, _ = peaks()
+    nccl_best, nccl_best_src = nccl_best_table(world)
     msg = 1 << 20
     with H.ClockSampler(local) as clk:
         per, calls, plan = measure(msg, "nvrar", args.steps, args.warmup)
     p50 = statistics.median(per)
     nccl_per, _, _ = measure(msg, "nccl", args.steps, args.warmup)
     nccl50 = statistics.median(nccl_per)
+    torch_per, _, _ = measure(msg, "torch", args.steps, args.warmup)
+    torch50 = statistics.median(torch_per)
 
     # e2e: pinned host input -> device, all-reduce, device -> host, per step; max over ranks
     ne = msg // 2
@@ -355,6 +427,16 @@ def run_multi(args, rank, world, local):
                    "blocks": pl[1], "speedup_vs_nccl": round(nv / v, 3),
                    "busbw_GBs": round(b_alg / (v * 1e-6) / 1e9, 1),
                    "roofline_us": round(rt, 3), "roofline_frac": round(rt / v, 3)}
+            best = nccl_best.get(size)
+            if best:
+                row.update(nccl_best_us=best["nccl_best_us"],
+                           nccl_best_cfg=f"{best['algo']}/{best['proto']} {best['version']}",
+                           speedup_vs_nccl_best=round(best["nccl_best_us"] / v, 3))
+            if not args.no_producer and size in PRODUCER_SIZES:
+                vp = statistics.median(measure(size, "nvrar", s_steps, 2, producer=True)[0])
+                npp = statistics.median(measure(size, "nccl", s_steps, 2, producer=True)[0])
+                row.update(nvrar_after_gemm_us=round(vp, 3), nccl_after_gemm_us=round(npp, 3),
+                           speedup_after_gemm=round(npp / vp, 3))
             if tuned is not None:
                 cands = tuned["measured"][size]
                 for a_name in ("hier", "twoshot", "oneshot", "mcast"):
@@ -365,6 +447,11 @@ def run_multi(args, rank, world, local):
 
     rt, b_alg = roof_us(msg)
     busbw = b_alg / (p50 * 1e-6) / 1e9
+    # the reference's CPU path on this host, same hierarchy, the message's
+    # element count (the reference has fp32 / int32 only), rank 0 only
+    cpu = cpu_reference(nodes, gpus, msg // 2, budget_s=10.0, max_calls=30) if rank == 0 else None
+    traffic, traffic_src = profiled_nvlink_traffic(world, plan[0], msg)
+    ncc.close()
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(p50, 3), "unit": "us", "n_gpus": world,
@@ -390,16 +477,23 @@ def run_multi(args, rank, world, local):
                        "p10_us": round(per[len(per) // 10], 3),
                        "p90_us": round(per[(9 * len(per)) // 10], 3),
                        "nccl_p50_us": round(nccl50, 3),
+                       "nccl": f"ncclAllReduce direct (libnccl {nccl_version}, default "
+                               f"algorithm/protocol), same graph methodology",
                        "speedup_vs_nccl": round(nccl50 / p50, 3),
+                       "torch_distributed_p50_us": round(torch50, 3),
+                       "nccl_best": nccl_best.get(msg),
+                       "nccl_best_source": nccl_best_src,
                        "alpha_signal_us": round(alpha, 3) if alpha else None},
             "roofline": {"bound": "nvlink", "achieved": round(busbw, 1),
                          "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
-                         "frac": round(busbw / NVLINK_PEAK_GBS, 4), "traffic": None,
+                         "frac": round(busbw / NVLINK_PEAK_GBS, 4), "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "algorithmic_bytes": b_alg,
                          "roofline_us": round(rt, 3), "time_frac": round(rt / p50, 4),
                          "note": "achieved = busbw 2(P-1)/P*M/t vs measured 770 GB/s peer copy; "
                                  "roofline_us = max(B_alg/900 GB/s, log2(P)*alpha_signal)"},
-            "cpu_baseline": None,
+            "cpu_baseline": {"value": round(cpu[0], 3), "unit": "us", "cores": cpu[2],
+                             "kind": cpu[1], "sample": cpu[3]},
             "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
                     "h2d_bytes_per_step": msg, "d2h_bytes_per_step": msg,
                     "path": "nvrar_allreduce_host (pinned host buffers, zero-copy)"},
@@ -423,6 +517,8 @@ def main():
     ap.add_argument("--no-autotune", action="store_true")
     ap.add_argument("--no-multicast", action="store_true",
                     help="do not set up the NVLS multicast one-shot candidate")
+    ap.add_argument("--no-producer", action="store_true",
+                    help="skip the GEMM-producer rows (all-reduce after a non-PDL kernel)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -838,8 +838,16 @@ static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, i
     const size_t upr = ((count * dtype_bytes(dtype) + 15) / 16 + nl - 1) / nl;
     // upt > 1 (host buffers over PCIe): fewer CTAs, each thread loops, so the
     // loads of unit i+1 overlap the stores of unit i across the link
+    static const int dev_upt = [] {  // units per thread on device buffers (tuning knob)
+      const char* e = getenv("NVRAR_DIRECT_UPT");
+      const int v = e ? atoi(e) : 1;
+      return v >= 1 && v <= 64 ? v : 1;
+    }();
+    const bool host = upt > 1;
+    if (!host) upt = dev_upt;
     const size_t full = (upr + kDirectThreads * upt - 1) / (kDirectThreads * upt);
-    const size_t spread = upt > 1 ? 1 : std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
+    const size_t spread = host || upt > 1 ? 1
+                                          : std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
     const size_t resident = std::max(1, c0->direct_ctas[dtype] / nl);
     blocks = static_cast<int>(std::max<size_t>(
         1, std::min<size_t>({std::max(full, spread), resident, static_cast<size_t>(kSeqSlots)})));

@@ -77,11 +77,12 @@ class Nccl:
     def unique_id(self) -> bytes:
         u = UniqueId()
         self._ck(self.lib.ncclGetUniqueId(ctypes.byref(u)), "ncclGetUniqueId")
-        return bytes(u.internal)
+        # not u.internal: a c_char array reads back as NUL-terminated bytes
+        return ctypes.string_at(ctypes.addressof(u), 128)
 
     def init_rank(self, nranks: int, uid: bytes, rank: int) -> None:
         u = UniqueId()
-        ctypes.memmove(u.internal, uid, 128)
+        ctypes.memmove(ctypes.addressof(u), uid, 128)
         self._ck(self.lib.ncclCommInitRank(ctypes.byref(self.comm), nranks, u, rank),
                  "ncclCommInitRank")
 

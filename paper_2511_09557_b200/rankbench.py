@@ -5,7 +5,7 @@ plane (barriers, max over ranks), the collective under test on the data path:
 
     python -m paper_2511_09557_b200.rankbench launch --world 2 --impl nvrar
     python -m paper_2511_09557_b200.rankbench launch --world 2 --impl nccl \
-        --nccl-lib system --nccl-algo Ring --nccl-proto LL
+        --nccl-lib system --nccl-algo Ring --nccl-proto LL   (NCCL_ALGO / NCCL_PROTO)
     python -m paper_2511_09557_b200.rankbench nccl-best --world 2      # every algo x proto x lib
 
 Timing (bench.py's rules): a step is one CUDA-graph replay of `calls`
@@ -59,6 +59,9 @@ def worker(args) -> None:
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = rank % max(1, torch.cuda.device_count()) if args.device < 0 else args.device
     torch.cuda.set_device(dev)
+    torch.zeros(1, device="cuda")  # the CUDA context exists from here on
+    if os.environ.get("RB_READY_DIR"):
+        open(os.path.join(os.environ["RB_READY_DIR"], f"ready{rank}"), "w").close()
     dist.init_process_group("gloo")
     nodes = args.nodes or (2 if world > 1 else 1)
     stream = torch.cuda.Stream()
@@ -168,14 +171,25 @@ def launch(args, extra_env=None) -> list:
         wargs.append("--autotune")
     if args.profile:
         wargs.append("--profile")
-    for r in range(args.world):
+    import tempfile
+    ready = tempfile.mkdtemp(prefix="rb_ready_")
+    # with a profiler on rank 0, the other ranks create their CUDA contexts
+    # first (a profiled process can hold up another process's CUDA init)
+    order = list(range(1, args.world)) + [0] if args.ncu_rank0 else list(range(args.world))
+    procs = [None] * args.world
+    for r in order:
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(args.world), LOCAL_RANK=str(r),
-                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), **(extra_env or {}))
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RB_READY_DIR=ready,
+                   **(extra_env or {}))
         cmd = [sys.executable, "-m", "paper_2511_09557_b200.rankbench", *wargs]
         if r == 0 and args.ncu_rank0:
+            t0 = time.time()
+            while not all(os.path.exists(os.path.join(ready, f"ready{q}"))
+                          for q in range(1, args.world)) and time.time() - t0 < 120:
+                time.sleep(0.1)
             cmd = shlex.split(args.ncu_rank0) + cmd
-        procs.append(subprocess.Popen(cmd, env=env, cwd=ROOT, stdout=subprocess.PIPE,
-                                      stderr=subprocess.STDOUT, text=True))
+        procs[r] = subprocess.Popen(cmd, env=env, cwd=ROOT, stdout=subprocess.PIPE,
+                                    stderr=subprocess.STDOUT, text=True)
     rows, outs = [], []
     for p in procs:
         try:
@@ -201,6 +215,7 @@ def nccl_best(args) -> None:
     best = {}
     allrows = []
     libs = args.nccl_libs.split(",")
+    args.impl = "nccl"
     for lib in libs:
         for algo in NCCL_ALGOS:
             for proto in NCCL_PROTOS:
@@ -238,6 +253,8 @@ def main() -> None:
     ap.add_argument("--producer", choices=["none", "gemm"], default="none")
     ap.add_argument("--nccl-lib", default="torch", help="torch | system | a path")
     ap.add_argument("--nccl-libs", default="system,torch")
+    ap.add_argument("--nccl-algo", default="")
+    ap.add_argument("--nccl-proto", default="")
     ap.add_argument("--device", type=int, default=-1)
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--ncu-rank0", default="")
@@ -248,7 +265,12 @@ def main() -> None:
     if args.mode == "worker":
         worker(args)
     elif args.mode == "launch":
-        for r in launch(args):
+        env = {}
+        if args.nccl_algo:
+            env["NCCL_ALGO"] = args.nccl_algo
+        if args.nccl_proto:
+            env["NCCL_PROTO"] = args.nccl_proto
+        for r in launch(args, env):
             print("RB " + json.dumps(r), flush=True)
     else:
         nccl_best(args)
