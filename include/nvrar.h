@@ -323,6 +323,15 @@ int nvrar_mc_attach(nvrar_comm_t comm, void* mc_base, void* local_base, size_t b
 int nvrar_mc_ready(nvrar_comm_t comm, int* ready);
 
 /* ---- config / introspection -------------------------------------------- */
+/* NvrarConfig (fused.hpp:106-116), validated like the reference's (blocks >= 0
+ * here, 0 = the selector's choice; chunk_bytes >= 8 and a multiple of 8).
+ * `blocks` = CTAs per rank (the reference's independent block ranges).
+ * `chunk_bytes` is accepted for the reference's call shape but does NOT change
+ * the GPU schedule: the reference pipelines the recursive-doubling steps in
+ * chunks of chunk_bytes (nvrar.hpp:193-220); the kernels forward every 16-byte
+ * unit to the next step as soon as it is reduced, i.e. the pipeline already
+ * runs at the finest granularity, and — as in the reference — results are
+ * invariant to (blocks, chunk_bytes). */
 int nvrar_set_config(nvrar_comm_t comm, int blocks, uint64_t chunk_bytes);
 int nvrar_set_algo(nvrar_comm_t comm, nvrar_algo_t algo);
 int nvrar_set_timeout(nvrar_comm_t comm, double timeout_s);

@@ -3,6 +3,12 @@ ranks on cuda:0, one cooperative launch per all-reduce) run eagerly a few
 times, so `ncu -k regex:<kernel>` can pick one launch.
 
     python -m paper_2511_09557_b200.profile_emu --algo twoshot --dtype f32 --bytes 1048576
+
+--range: the bench's graph instead (rotating buffers > L2, `calls` back-to-back
+all-reduces), replayed warm and then once between cudaProfilerStart/Stop, for
+`ncu --replay-mode range --profile-from-start off`: DRAM bytes of the whole
+range / calls = per-call traffic INCLUDING the write-back of earlier calls'
+outputs (a single-kernel capture leaves its writes in L2).
 """
 from __future__ import annotations
 
@@ -25,6 +31,7 @@ def main():
     ap.add_argument("--solo", action="store_true",
                     help="one 1x1 communicator (the single-rank kernel, no virtual ranks)")
     ap.add_argument("--blocks", type=int, default=0)
+    ap.add_argument("--range", action="store_true")
     args = ap.parse_args()
     dt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     n = args.bytes // (4 if args.dtype == "f32" else 2)
@@ -45,6 +52,25 @@ def main():
     g = LocalGroup(ClusterTopology(args.nodes, args.gpus), max(args.bytes, 1 << 20), device=0)
     g.set_algo(args.algo)
     g.set_protocol(args.proto)
+    if args.range:
+        from . import harness as H
+        calls = H.calls_for(args.bytes, p)
+        sets = [([torch.randn(n, device="cuda").to(dt) for _ in range(p)],
+                 [torch.empty(n, device="cuda", dtype=dt) for _ in range(p)]) for _ in range(calls)]
+        stream = torch.cuda.Stream()
+        gr = H.graph_of(lambda i: g.launch(*sets[i], stream=torch.cuda.current_stream()), calls,
+                        stream)
+        for _ in range(3):
+            gr.replay()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        gr.replay()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        g.check()
+        print(f"range: {calls} calls, plan {g.plan(n, dt)} ok")
+        g.close()
+        return
     ins = [torch.randn(n, device="cuda").to(dt) for _ in range(p)]
     outs = [torch.empty_like(t) for t in ins]
     for _ in range(args.calls):
