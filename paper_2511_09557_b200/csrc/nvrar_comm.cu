@@ -101,6 +101,7 @@ struct nvrar_comm {
   int direct_ctas[3] = {148, 148, 148};  // co-resident direct-schedule CTAs per dtype
   bool pdl = true;     // programmatic dependent launch for single-rank launches
   int proto = NVRAR_PROTO_AUTO;
+  int flags = 0;  // LaunchParams.flags (schedule variants; NVRAR_FLAGS)
   int threads = kThreads;  // threads per CTA (multiple of 32, <= kThreads)
   uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
   uint32_t canary_base[kMaxRanks] = {};  // per-peer canary flag base (same on both sides)
@@ -378,6 +379,7 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
     c->direct_ctas[dt] = sms * std::max(o, 1);
   }
   if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
+  if (const char* v = getenv("NVRAR_FLAGS")) c->flags = atoi(v) & (kFlagEarlySeq | kFlagLazyLen);
   if (const char* v = getenv("NVRAR_THREADS")) {
     const int t = atoi(v);
     if (t >= 32 && t <= kThreads && t % 32 == 0) c->threads = t;
@@ -941,6 +943,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   lp.count = count;
   lp.e_off = e_off;
   lp.n_order = n_order;
+  lp.flags = c0->flags;
   CUDA_TRY(c0, cudaSetDevice(c0->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (count == 0) {

@@ -132,7 +132,20 @@ struct LaunchParams {
   // n_order = 0: the launch is the whole vector. Flat and direct kernels only.
   uint64_t e_off;
   uint64_t n_order;
+  // Schedule variants (bit flags, kFlag*): where the call counter is written
+  // back and where the flat schedules check the peers' lengths.
+  int flags;
 };
+
+// kFlagEarlySeq: each CTA writes its call-counter slots right after reading
+//   its own (nothing in this launch reads them again; the next launch reads
+//   them after griddepcontrol.wait), taking those stores off the kernel tail.
+// kFlagLazyLen: the flat schedules (one rank per launch) do not wait for the
+//   peers' (seq, len) words before reducing; the length check runs at the end
+//   of the call — before it completes, so a mismatch still faults the call
+//   (sticky: later launches return at entry) — and a wait on a shorter peer's
+//   missing data is diagnosed as the length mismatch it is.
+enum : int { kFlagEarlySeq = 1, kFlagLazyLen = 2 };
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):
 //   NVRAR — ring fold of the node's ranks per G-chunk, pairwise tree over nodes;
@@ -216,6 +229,10 @@ struct Ctl {
   bool aborted;
   int phase;
   bool last_chance;
+  // kFlagLazyLen: this rank's counters (peer p's (seq<<32)|len at [p]) and
+  // the call's length, consulted when a data wait stalls
+  const uint64_t* len_words;
+  uint32_t len;
 };
 
 __device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, int peer,
@@ -243,6 +260,14 @@ __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t w
   if (ld_volatile32(&c.st->err.code) != 0u) {
     c.aborted = true;
     return true;
+  }
+  if (c.len_words != nullptr && kind == kFlagWait && peer >= 0 && (c.spins & 4095u) == 0u) {
+    // a data wait that lasts: is the peer in this call with another length?
+    const uint64_t v = ld_volatile64(c.len_words + peer);
+    if (static_cast<uint32_t>(v >> 32) == c.seq && static_cast<uint32_t>(v) != c.len) {
+      record_fault(c, kProtocolFault, kLenMismatch, peer, 0, v);
+      return true;
+    }
   }
   const uint64_t now = globaltimer();
   if (now - c.t0 > c.timeout_ns) {

@@ -117,6 +117,8 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, SeqWords w)
   c.spins = 0;
   c.aborted = false;
   c.last_chance = false;
+  c.len_words = nullptr;
+  c.len = 0;
   c.t0 = globaltimer();
   c.seq = s_seq + 1u;
   c.phase = 2;
@@ -254,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   Ctl c;
   if (!begin_seq(d, c, sw)) return;  // sticky fault: comm is dead
   const uint32_t parity = c.seq & 1u;
+  if (lp.flags & kFlagEarlySeq) end_call(d, c.seq);
 
   // Peer-only sync, publish half (nvrar.hpp:163-171).
   if (kSteps > 0 && blockIdx.x == 0 && threadIdx.x < kSteps) {
@@ -497,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
   }
   stamp(d, 5);
-  end_call(d, c.seq);
+  if (!(lp.flags & kFlagEarlySeq)) end_call(d, c.seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -572,6 +575,12 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   Ctl c;
   if (!begin_seq(d, c, sw)) return;
   const uint32_t parity = c.seq & 1u;
+  const bool lazy_len = !EMU && (lp.flags & kFlagLazyLen) != 0;
+  if (lp.flags & kFlagEarlySeq) end_call(d, c.seq);
+  if (lazy_len) {
+    c.len_words = counters(d, me);
+    c.len = static_cast<uint32_t>(n);
+  }
 
   if (blockIdx.x == 0) {
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
@@ -643,10 +652,12 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   stamp(d, 2);
   c.phase = 3;
 
-  for (int p = threadIdx.x; p < P; p += blockDim.x) {
-    if (p != me) wait_seq_len(c, d, p, n);
+  if (!lazy_len) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      if (p != me) wait_seq_len(c, d, p, n);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   stamp(d, 3);
   c.phase = 4;
 
@@ -658,6 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   uint8_t* const a_mine = (mc ? d.mc_local : d.base[me] + d.lay.a_off) +
                           static_cast<uint64_t>(parity) * d.world * d.lay.a_src * 8;
   const uint64_t a_stride = d.lay.a_src * 8;
+  uint64_t len_seen = 0;
   for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
     const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
@@ -701,6 +713,10 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       }
     }
     recv_grid<Raw, RDW, N, MAXG>(c, slots, u, r, pending, src);
+    if (lazy_len && u == u_first && threadIdx.x < P) {
+      // the peer's (seq, len) word, read now that its data is here; used at the end
+      len_seen = ld_volatile64(counters(d, me) + threadIdx.x);
+    }
     const int c3 = straddle ? c0 + 1 : c0;
 
     // Node partials, combined on the fly into the pairwise tree over nodes
@@ -807,8 +823,24 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
       }
     }
   }
+  if (lazy_len) {
+    // the peers' (seq, len) words, published before their data, were read
+    // after it arrived: usually no wait is left
+    c.phase = 3;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      if (p == me) continue;
+      const uint64_t v = p == static_cast<int>(threadIdx.x) ? len_seen : 0ull;
+      if (static_cast<uint32_t>(v >> 32) == c.seq) {
+        if ((v & 0xFFFFFFFFull) != (n & 0xFFFFFFFFull)) {
+          record_fault(c, kProtocolFault, kLenMismatch, p, 0, v);
+        }
+      } else {
+        wait_seq_len(c, d, p, n);
+      }
+    }
+  }
   stamp(d, 5);
-  end_call(d, c.seq);
+  if (!(lp.flags & kFlagEarlySeq)) end_call(d, c.seq);
 }
 
 // ---------------------------------------------------------------------------
