@@ -4,11 +4,13 @@ times, so `ncu -k regex:<kernel>` can pick one launch.
 
     python -m paper_2511_09557_b200.profile_emu --algo twoshot --dtype f32 --bytes 1048576
 
---range: the bench's graph instead (rotating buffers > L2, `calls` back-to-back
-all-reduces), replayed warm and then once between cudaProfilerStart/Stop, for
-`ncu --replay-mode range --profile-from-start off`: DRAM bytes of the whole
-range / calls = per-call traffic INCLUDING the write-back of earlier calls'
-outputs (a single-kernel capture leaves its writes in L2).
+--rotate: the bench's rotating buffer sets (> L2), launched eagerly twice over:
+profile the second pass with `ncu --cache-control none`, so each launch's DRAM
+counters include the write-back of earlier calls' outputs that it evicts (a
+single cold-cache capture leaves its own writes in L2): sum / launches = the
+per-call DRAM traffic in steady state. (--range: the same inside a CUDA graph
+between cudaProfilerStart/Stop; ncu's range replay does not accept graph
+launches on this driver.)
 """
 from __future__ import annotations
 
@@ -32,6 +34,7 @@ def main():
                     help="one 1x1 communicator (the single-rank kernel, no virtual ranks)")
     ap.add_argument("--blocks", type=int, default=0)
     ap.add_argument("--range", action="store_true")
+    ap.add_argument("--rotate", action="store_true")
     args = ap.parse_args()
     dt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     n = args.bytes // (4 if args.dtype == "f32" else 2)
@@ -52,6 +55,19 @@ def main():
     g = LocalGroup(ClusterTopology(args.nodes, args.gpus), max(args.bytes, 1 << 20), device=0)
     g.set_algo(args.algo)
     g.set_protocol(args.proto)
+    if args.rotate:
+        from . import harness as H
+        calls = H.calls_for(args.bytes, p)
+        sets = [([torch.randn(n, device="cuda").to(dt) for _ in range(p)],
+                 [torch.empty(n, device="cuda", dtype=dt) for _ in range(p)]) for _ in range(calls)]
+        for _ in range(2):
+            for i in range(calls):
+                g.launch(*sets[i])
+        torch.cuda.synchronize()
+        g.check()
+        print(f"rotate: 2 x {calls} calls, plan {g.plan(n, dt)} ok")
+        g.close()
+        return
     if args.range:
         from . import harness as H
         calls = H.calls_for(args.bytes, p)
