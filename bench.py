@@ -57,9 +57,10 @@ def nccl_best_table(world):
 
 
 def profiled_nvlink_traffic(world, algo, msg):
-    """NVLink bytes (TX + RX) per launch of the schedule's kernel at this size and
-    world, from the committed single-pass ncu capture of rank 0
-    (profiles/*ncu_nvlink*.json), or None."""
+    """NVLink egress bytes per launch per GPU (nvltx__bytes: payload + link
+    protocol) of the schedule's kernel at this size and world, from the committed
+    single-pass ncu capture of rank 0 (profiles/*ncu_nvlink*.json), or None.
+    Ingress equals the peers' egress (symmetric schedules)."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_nvlink*.json")),
                        reverse=True):
@@ -68,7 +69,7 @@ def profiled_nvlink_traffic(world, algo, msg):
                 p = json.load(fh)
             for r in p["rows"]:
                 if r["world"] == world and r["algo"] == algo and r["bytes"] == msg:
-                    return int(r["nvl_tx_bytes"] + r["nvl_rx_bytes"]), os.path.basename(path)
+                    return int(r["nvl_tx_bytes"]), os.path.basename(path)
         except Exception:
             continue
     return None, None
@@ -488,6 +489,8 @@ def run_multi(args, rank, world, local):
                          "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                          "frac": round(busbw / NVLINK_PEAK_GBS, 4), "traffic": traffic,
                          "traffic_source": traffic_src,
+                         "traffic_note": "NVLink egress bytes per launch per GPU (ncu nvltx__bytes, "
+                                         "payload + link protocol) vs algorithmic_bytes",
                          "algorithmic_bytes": b_alg,
                          "roofline_us": round(rt, 3), "time_frac": round(rt / p50, 4),
                          "note": "achieved = busbw 2(P-1)/P*M/t vs measured 770 GB/s peer copy; "

@@ -18,7 +18,8 @@
 
 namespace nvrar {
 using KernelFn = void (*)(LaunchParams);
-KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport);
+KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport,
+                       bool fast = false);
 KernelFn bump_kernel();
 KernelFn select_direct(int dtype, int nodes, int gpus);
 KernelFn select_phase(int dtype, int mode, int nodes, bool emu);
@@ -102,6 +103,7 @@ struct nvrar_comm {
   bool pdl = true;     // programmatic dependent launch for single-rank launches
   int proto = NVRAR_PROTO_AUTO;
   int flags = 0;  // LaunchParams.flags (schedule variants; NVRAR_FLAGS)
+  bool fast_oneshot = true;  // one-shot calls run the specialised kernel (SHOT = 1)
   int threads = kThreads;  // threads per CTA (multiple of 32, <= kThreads)
   uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
   uint32_t canary_base[kMaxRanks] = {};  // per-peer canary flag base (same on both sides)
@@ -379,6 +381,7 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
     c->direct_ctas[dt] = sms * std::max(o, 1);
   }
   if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
+  if (const char* v = getenv("NVRAR_FAST_ONESHOT")) c->fast_oneshot = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_FLAGS")) c->flags = atoi(v) & (kFlagEarlySeq | kFlagLazyLen);
   if (const char* v = getenv("NVRAR_THREADS")) {
     const int t = atoi(v);
@@ -1003,7 +1006,10 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
                         : select_kernel(dtype, algo != NVRAR_ALGO_HIER,
                                         order == NVRAR_ORDER_RING ? 1 : c0->nodes,
                                         order == NVRAR_ORDER_RING ? c0->world : c0->gpus, emu,
-                                        lamport);
+                                        lamport,
+                                        // the one-shot specialisation (NVRAR_FAST_ONESHOT=0: off)
+                                        c0->fast_oneshot && algo == NVRAR_ALGO_ONESHOT &&
+                                            order == NVRAR_ORDER_NVRAR && !mc);
   if (!k) return fail(c0, NVRAR_ERR_INTERNAL, "no kernel for nodes=%d", c0->nodes);
 
   cudaLaunchConfig_t cfg{};
@@ -1532,57 +1538,6 @@ static int host_allreduce(nvrar_comm_t* comms, int nc, const void* const* hsend,
                                                                     c0->max_bytes / eb / 16 * 16))
                             : std::max<size_t>(count, 1);
   const size_t nch = count == 0 ? 1 : (count + ce - 1) / ce;
-  // Split-direction pipeline for a local group holding EVERY rank (no other
-  // process shares its call sequence, so its windowing is free): the copy
-  // engine moves the inputs host->device (DMA, the slower PCIe direction on
-  // this platform) window by window into device staging, and each window's
-  // kernel writes its results straight into the pinned outputs (posted
-  // zero-copy writes on the device->host direction), so the two directions of
-  // the link overlap. NVRAR_HOST_MODE=zerocopy keeps the all-zero-copy path.
-  static const int host_mode = [] {
-    const char* e = getenv("NVRAR_HOST_MODE");
-    return e && std::string(e) == "zerocopy" ? 0 : 1;
-  }();
-  static const size_t split_chunk = [] {
-    const char* e = getenv("NVRAR_SPLIT_CHUNK");
-    const long long v = e ? atoll(e) : 0;
-    return v >= 4096 ? static_cast<size_t>(v) : static_cast<size_t>(128 << 10);
-  }();
-  if (mapped && !c0->host_chunk && host_mode == 1 && local_group && nc == c0->world &&
-      nch == 1 && windows && count * eb > split_chunk) {
-    const size_t we = std::max<size_t>(16 / eb, split_chunk / eb / 16 * 16);
-    const size_t nw = (count + we - 1) / we;
-    const size_t wbytes = we * eb;
-    for (int i = 0; i < nc; ++i) {
-      if (int rc = host_pipe_ready(comms[i], wbytes)) return rc;
-    }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    std::vector<const void*> ws(nc);
-    std::vector<void*> wr(nc);
-    CUDA_TRY(c0, cudaEventRecord(c0->ev_start, s));
-    CUDA_TRY(c0, cudaStreamWaitEvent(c0->s_h2d, c0->ev_start, 0));
-    for (size_t i = 0; i < nw; ++i) {
-      const int b = static_cast<int>(i & 1);
-      const size_t off = i * we, cnt = std::min(we, count - off);
-      // staging buffer b is free once the kernel of window i-2 has read it
-      if (i >= 2) CUDA_TRY(c0, cudaStreamWaitEvent(c0->s_h2d, c0->ev_ar[b], 0));
-      for (int r = 0; r < nc; ++r) {
-        uint8_t* din = comms[r]->stage + b * wbytes;
-        CUDA_TRY(c0, cudaMemcpyAsync(din, static_cast<const uint8_t*>(hsend[r]) + off * eb,
-                                     cnt * eb, cudaMemcpyHostToDevice, c0->s_h2d));
-        ws[r] = din;
-        wr[r] = static_cast<uint8_t*>(zrecv[r]) + off * eb;
-      }
-      CUDA_TRY(c0, cudaEventRecord(c0->ev_h2d[b], c0->s_h2d));
-      CUDA_TRY(c0, cudaStreamWaitEvent(s, c0->ev_h2d[b], 0));
-      if (int rc = launch(comms, nc, ws.data(), wr.data(), cnt, dtype, op, stream, ~0ull,
-                          local_group, NVRAR_PHASE_ALL, NVRAR_ORDER_NVRAR, nullptr, off, count)) {
-        return rc;
-      }
-      CUDA_TRY(c0, cudaEventRecord(c0->ev_ar[b], s));
-    }
-    return NVRAR_SUCCESS;
-  }
   if (mapped && !c0->host_chunk) {
     // zero-copy (unless a chunk was asked for, which means staging): the same
     // windows, straight over the mapped host memory

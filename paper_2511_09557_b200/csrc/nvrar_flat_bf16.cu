@@ -3,8 +3,8 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_flat_bf16(int nodes, int gpus, bool emu, bool lamport) {
-  return lamport ? flat_kernel_for<BF16, true>(nodes, gpus, emu)
-                 : flat_kernel_for<BF16, false>(nodes, gpus, emu);
+KernelFn kernel_flat_bf16(int nodes, int gpus, bool emu, bool lamport, bool fast) {
+  return lamport ? flat_kernel_for<BF16, true>(nodes, gpus, emu, fast)
+                 : flat_kernel_for<BF16, false>(nodes, gpus, emu, fast);
 }
 }  // namespace nvrar

@@ -3,8 +3,8 @@
 #include "nvrar_kernels.cuh"
 
 namespace nvrar {
-KernelFn kernel_flat_i32(int nodes, int gpus, bool emu, bool lamport) {
-  (void)lamport;
-  return flat_kernel_for<I32, false>(nodes, gpus, emu);
+KernelFn kernel_flat_i32(int nodes, int gpus, bool emu, bool lamport, bool fast) {
+  return lamport ? flat_kernel_for<I32, true>(nodes, gpus, emu, fast)
+                 : flat_kernel_for<I32, false>(nodes, gpus, emu, fast);
 }
 }  // namespace nvrar

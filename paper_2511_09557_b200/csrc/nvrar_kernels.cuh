@@ -525,7 +525,11 @@ __device__ __forceinline__ typename E::acc pick(const uint32_t (&r)[N][MAXG][RDW
   return v;
 }
 
-template <class E, bool LAMPORT, int N, int MAXG, bool EMU>
+// SHOT = 0: schedule, order and multicast chosen at run time (LaunchParams);
+// SHOT = 1: the small-message specialisation — one-shot, NVRAR order, unicast —
+// with the two-shot, ring/tree and multicast code compiled out (a smaller
+// kernel: fewer instruction-fetch stalls at the start of every call).
+template <class E, bool LAMPORT, int N, int MAXG, bool EMU, int SHOT = 0>
 __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant__ LaunchParams lp) {
   using A = typename E::acc;
   using C = Cfg<E, LAMPORT>;
@@ -536,8 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const RankDesc& d = rank_desc<EMU>(lp);
   const uint64_t n = lp.count;
   const int G = d.gpus, P = d.world, me = d.rank;
-  const bool oneshot = lp.oneshot != 0;
-  const int order = lp.order;
+  const bool oneshot = SHOT == 1 ? true : lp.oneshot != 0;
+  const int order = SHOT == 1 ? static_cast<int>(kOrderNvrar) : lp.order;
   // members of one fold: the node's G ranks, or (ring order) all P ranks
   const int OG = order == kOrderRing ? P : G;
   const uint64_t n_ord = lp.n_order ? lp.n_order : n;  // order follows the whole vector
@@ -560,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   // Prefetch this thread's first unit of every sub-shard (pre[j]: owner
   // (me + j) % P; j = 0 is our own) before the call number is read. One-shot
   // sends the same unit to everyone, so it loads once.
-  constexpr int kPre = 8;
+  constexpr int kPre = N * MAXG < 8 ? N * MAXG : 8;  // ranks <= N * MAXG
   uint32_t pre[kPre][RDW];
   int pv[kPre];
 #pragma unroll
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   // Reduce-scatter pushes: the owner q of each sub-shard receives our copy.
   // Multicast one-shot: ONE store per cell to the multicast mapping reaches
   // slot `me` of every rank's multicast A area (the NVSwitch replicates it).
-  const bool mc = lp.mc != 0;
+  const bool mc = SHOT == 1 ? false : lp.mc != 0;
   uint4* const mc_slot = mc ? reinterpret_cast<uint4*>(
                                   d.mc + (static_cast<uint64_t>(parity) * d.world + me) * d.lay.a_src * 8)
                             : nullptr;
@@ -1189,32 +1193,34 @@ KernelFn hier_for(int nodes, int gpus) {
 // Flat kernels are specialised on MAXG = the next power of two >= gpus per node
 // (register tiles r[N][MAXG] sized to the topology: a 2x1 launch must not
 // carry the 2x8 tile — measured +1.5 us per call at P=2). N * MAXG <= 16.
-template <class E, bool LAMPORT, bool EMU, int N>
+template <class E, bool LAMPORT, bool EMU, int N, int SHOT>
 KernelFn flat_for_n(int gpus) {
-  if (gpus <= 1) return flat_kernel<E, LAMPORT, N, 1, EMU>;
-  if (gpus <= 2) return flat_kernel<E, LAMPORT, N, 2, EMU>;
+  if (gpus <= 1) return flat_kernel<E, LAMPORT, N, 1, EMU, SHOT>;
+  if (gpus <= 2) return flat_kernel<E, LAMPORT, N, 2, EMU, SHOT>;
   if constexpr (N <= 4) {
-    if (gpus <= 4) return flat_kernel<E, LAMPORT, N, 4, EMU>;
+    if (gpus <= 4) return flat_kernel<E, LAMPORT, N, 4, EMU, SHOT>;
   }
   if constexpr (N <= 2) {
-    if (gpus <= 8) return flat_kernel<E, LAMPORT, N, 8, EMU>;
+    if (gpus <= 8) return flat_kernel<E, LAMPORT, N, 8, EMU, SHOT>;
   }
   return nullptr;
 }
 
-template <class E, bool LAMPORT, bool EMU>
+template <class E, bool LAMPORT, bool EMU, int SHOT = 0>
 KernelFn flat_for(int nodes, int gpus) {
   switch (nodes) {
-    case 1: return flat_for_n<E, LAMPORT, EMU, 1>(gpus);
-    case 2: return flat_for_n<E, LAMPORT, EMU, 2>(gpus);
-    case 4: return flat_for_n<E, LAMPORT, EMU, 4>(gpus);
-    case 8: return flat_for_n<E, LAMPORT, EMU, 8>(gpus);
+    case 1: return flat_for_n<E, LAMPORT, EMU, 1, SHOT>(gpus);
+    case 2: return flat_for_n<E, LAMPORT, EMU, 2, SHOT>(gpus);
+    case 4: return flat_for_n<E, LAMPORT, EMU, 4, SHOT>(gpus);
+    case 8: return flat_for_n<E, LAMPORT, EMU, 8, SHOT>(gpus);
     default: return nullptr;
   }
 }
 
+// fast: the one-shot specialisation (SHOT = 1), per-rank launches only
 template <class E, bool LAMPORT>
-KernelFn flat_kernel_for(int nodes, int gpus, bool emu) {
+KernelFn flat_kernel_for(int nodes, int gpus, bool emu, bool fast = false) {
+  if (fast && !emu) return flat_for<E, LAMPORT, false, 1>(nodes, gpus);
   return emu ? flat_for<E, LAMPORT, true>(nodes, gpus) : flat_for<E, LAMPORT, false>(nodes, gpus);
 }
 
@@ -1226,9 +1232,9 @@ KernelFn hier_kernel_for(int nodes, int gpus, bool emu) {
 KernelFn kernel_hier_f32(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_hier_bf16(int nodes, int gpus, bool emu, bool lamport);
 KernelFn kernel_hier_i32(int nodes, int gpus, bool emu, bool lamport);
-KernelFn kernel_flat_f32(int nodes, int gpus, bool emu, bool lamport);
-KernelFn kernel_flat_bf16(int nodes, int gpus, bool emu, bool lamport);
-KernelFn kernel_flat_i32(int nodes, int gpus, bool emu, bool lamport);
+KernelFn kernel_flat_f32(int nodes, int gpus, bool emu, bool lamport, bool fast);
+KernelFn kernel_flat_bf16(int nodes, int gpus, bool emu, bool lamport, bool fast);
+KernelFn kernel_flat_i32(int nodes, int gpus, bool emu, bool lamport, bool fast);
 KernelFn kernel_direct_f32(int nodes, int gpus);
 KernelFn kernel_direct_bf16(int nodes, int gpus);
 KernelFn kernel_direct_i32(int nodes, int gpus);

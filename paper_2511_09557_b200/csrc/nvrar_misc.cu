@@ -92,11 +92,12 @@ __global__ void canary_kernel(const __grid_constant__ LaunchParams lp, int peer,
 using CanaryFn = void (*)(LaunchParams, int, int, int, uint32_t, uint32_t, uint32_t, uint32_t*);
 CanaryFn canary_fn() { return canary_kernel; }
 
-KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport) {
+KernelFn select_kernel(int dtype, bool flat, int nodes, int gpus, bool emu, bool lamport,
+                       bool fast) {
   switch (dtype) {
-    case 0: return flat ? kernel_flat_i32(nodes, gpus, emu, false) : kernel_hier_i32(nodes, gpus, emu, false);
-    case 1: return flat ? kernel_flat_f32(nodes, gpus, emu, lamport) : kernel_hier_f32(nodes, gpus, emu, lamport);
-    case 2: return flat ? kernel_flat_bf16(nodes, gpus, emu, lamport) : kernel_hier_bf16(nodes, gpus, emu, lamport);
+    case 0: return flat ? kernel_flat_i32(nodes, gpus, emu, false, fast) : kernel_hier_i32(nodes, gpus, emu, false);
+    case 1: return flat ? kernel_flat_f32(nodes, gpus, emu, lamport, fast) : kernel_hier_f32(nodes, gpus, emu, lamport);
+    case 2: return flat ? kernel_flat_bf16(nodes, gpus, emu, lamport, fast) : kernel_hier_bf16(nodes, gpus, emu, lamport);
     default: return nullptr;
   }
 }
