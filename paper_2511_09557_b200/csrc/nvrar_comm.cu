@@ -856,6 +856,11 @@ static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, i
     const size_t resident = std::max(1, c0->direct_ctas[dtype] / nl);
     blocks = static_cast<int>(std::max<size_t>(
         1, std::min<size_t>({std::max(full, spread), resident, static_cast<size_t>(kSeqSlots)})));
+    static const int dev_ctas = [] {  // CTAs per rank on device buffers (tuning knob)
+      const char* e = getenv("NVRAR_DIRECT_CTAS");
+      return e ? atoi(e) : 0;
+    }();
+    if (!host && dev_ctas > 0) blocks = std::min(dev_ctas, static_cast<int>(resident));
   } else if (emu) {
     blocks = std::max(1, std::min(blocks, c0->max_ctas / nl));
   }
