@@ -851,8 +851,12 @@ static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, i
     const bool host = upt > 1;
     if (!host) upt = dev_upt;
     const size_t full = (upr + kDirectThreads * upt - 1) / (kDirectThreads * upt);
+    // two CTAs per SM over the whole launch (measured at 2x4, 1 MB fp32:
+    // 1 / 2 / 4 per SM -> 6.17 / 5.11 / 5.28 us; the round-1 rule, 256 CTAs,
+    // left 40 SMs with one CTA and 108 with two: 5.23 us)
     const size_t spread = host || upt > 1 ? 1
-                                          : std::min<size_t>((c0->sms + nl - 1) / nl, (upr + 31) / 32);
+                                          : std::min<size_t>((2 * c0->sms + nl - 1) / nl,
+                                                             (upr + 31) / 32);
     const size_t resident = std::max(1, c0->direct_ctas[dtype] / nl);
     blocks = static_cast<int>(std::max<size_t>(
         1, std::min<size_t>({std::max(full, spread), resident, static_cast<size_t>(kSeqSlots)})));

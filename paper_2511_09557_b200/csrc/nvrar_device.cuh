@@ -235,21 +235,56 @@ struct Ctl {
   uint32_t len;
 };
 
-__device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, int peer,
-                                             uint64_t word, uint64_t observed) {
-  ErrRec* e = &c.st->err;
+// The fault and watchdog paths are out of line (__noinline__): they are cold,
+// and inlined at every poll site they made the kernels several times larger —
+// the hot path then spread over more instruction-cache lines (no_instruction
+// stalls dominated the one-shot's profile, profiles/r02_ncu_nvlink_p2.json).
+static __device__ __noinline__ void record_fault_at(RankState* st, uint32_t code, int kind, int peer,
+                                             uint32_t seq, uint64_t word, uint64_t observed,
+                                             int phase) {
+  ErrRec* e = &st->err;
   if (atomicCAS(&e->code, 0u, 0xFFFFFFFFu) == 0u) {
     e->kind = kind;
     e->peer = peer;
-    e->expected = c.seq;
+    e->expected = seq;
     e->word = word;
     e->observed = observed;
-    e->phase = c.phase;
+    e->phase = phase;
     e->cta = static_cast<int32_t>(blockIdx.x);
     __threadfence();
     atomicExch(&e->code, code);
   }
+}
+
+__device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, int peer,
+                                             uint64_t word, uint64_t observed) {
+  record_fault_at(c.st, code, kind, peer, c.seq, word, observed, c.phase);
   c.aborted = true;
+}
+
+// The watchdog's periodic check: 0 = keep waiting, 1 = give up (a fault is
+// recorded, here or by another thread), 2 = the deadline passed once (poll one
+// more full round before declaring a deadlock: a thread can be descheduled
+// between its poll and this check).
+static __device__ __noinline__ int wait_check(RankState* st, uint64_t t0, uint64_t timeout_ns,
+                                       int last_chance, const uint64_t* len_words, uint32_t len,
+                                       uint32_t spins, uint32_t seq, int phase, int kind, int peer,
+                                       uint64_t word, uint64_t observed) {
+  if (ld_volatile32(&st->err.code) != 0u) return 1;
+  if (len_words != nullptr && kind == kFlagWait && peer >= 0 && (spins & 4095u) == 0u) {
+    // a data wait that lasts: is the peer in this call with another length?
+    const uint64_t v = ld_volatile64(len_words + peer);
+    if (static_cast<uint32_t>(v >> 32) == seq && static_cast<uint32_t>(v) != len) {
+      record_fault_at(st, kProtocolFault, kLenMismatch, peer, seq, 0, v, phase);
+      return 1;
+    }
+  }
+  if (globaltimer() - t0 > timeout_ns) {
+    if (!last_chance) return 2;
+    record_fault_at(st, kDeadlock, kind, peer, seq, word, observed, phase);
+    return 1;
+  }
+  return 0;
 }
 
 // Called while a wait is unsatisfied. Returns true when the thread must give up.
@@ -257,29 +292,15 @@ __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t w
                                           uint64_t observed) {
   if (c.aborted) return true;
   if ((++c.spins & 127u) != 0u) return false;
-  if (ld_volatile32(&c.st->err.code) != 0u) {
+  const int r = wait_check(c.st, c.t0, c.timeout_ns, c.last_chance ? 1 : 0, c.len_words, c.len,
+                           c.spins, c.seq, c.phase, kind, peer, word, observed);
+  if (r == 1) {
     c.aborted = true;
     return true;
   }
-  if (c.len_words != nullptr && kind == kFlagWait && peer >= 0 && (c.spins & 4095u) == 0u) {
-    // a data wait that lasts: is the peer in this call with another length?
-    const uint64_t v = ld_volatile64(c.len_words + peer);
-    if (static_cast<uint32_t>(v >> 32) == c.seq && static_cast<uint32_t>(v) != c.len) {
-      record_fault(c, kProtocolFault, kLenMismatch, peer, 0, v);
-      return true;
-    }
-  }
-  const uint64_t now = globaltimer();
-  if (now - c.t0 > c.timeout_ns) {
-    // A thread can be descheduled between its poll and this check; declare a
-    // deadlock only if the wait is still unsatisfied after one more full round.
-    if (!c.last_chance) {
-      c.last_chance = true;
-      c.spins |= 127u;
-      return false;
-    }
-    record_fault(c, kDeadlock, kind, peer, word, observed);
-    return true;
+  if (r == 2) {
+    c.last_chance = true;
+    c.spins |= 127u;
   }
   return false;
 }
@@ -297,11 +318,15 @@ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   return x;
 }
 
+static __device__ __noinline__ void jitter_sleep(uint32_t seed, uint32_t key, uint32_t max_ns) {
+  __nanosleep(mix32(seed ^ mix32(key)) % max_ns);
+}
+
 __device__ __forceinline__ void poll_pause(const Ctl& c) {
   __nanosleep(c.poll_ns ? c.poll_ns : 32u);
   if (c.jitter_ns) {
-    __nanosleep(mix32(c.jitter_seed ^ mix32(c.spins * 0x9E3779B9u ^ threadIdx.x ^
-                                            (blockIdx.x << 16))) % c.jitter_ns);
+    jitter_sleep(c.jitter_seed, c.spins * 0x9E3779B9u ^ threadIdx.x ^ (blockIdx.x << 16),
+                 c.jitter_ns);
   }
 }
 
@@ -309,10 +334,10 @@ __device__ __forceinline__ void poll_pause(const Ctl& c) {
 // whole warp (per CTA, warp, unit group and site), different per seed.
 __device__ __forceinline__ void jitter(const Ctl& c, uint32_t site) {
   if (c.jitter_ns == 0) return;
-  const uint32_t h = mix32(c.jitter_seed ^ mix32(c.seq * 0x9E3779B9u ^ (blockIdx.x << 20) ^
-                                                 (blockIdx.y << 26) ^ ((threadIdx.x >> 5) << 8) ^
-                                                 site));
-  __nanosleep(h % c.jitter_ns);
+  jitter_sleep(c.jitter_seed,
+               c.seq * 0x9E3779B9u ^ (blockIdx.x << 20) ^ (blockIdx.y << 26) ^
+                   ((threadIdx.x >> 5) << 8) ^ site,
+               c.jitter_ns);
 }
 
 // flag observed in a slot for call `seq`: equal = arrived; behind = not yet
