@@ -104,3 +104,26 @@ def test_eight_rank_layout_on_fewer_gpus(nodes, gpus):
     rc, out = _run(8, nodes, gpus, ("--dev-mod", "4", "--quick"))
     assert rc == 0, out[-4000:]
     assert out.count(": OK") == 8, out[-4000:]
+
+
+@pytest.mark.parametrize("world,nodes,gpus", [(2, 2, 1), (4, 2, 2), (4, 4, 1)])
+def test_multigpu_registered_fuzz_ops(world, nodes, gpus):
+    """One rank per GPU over NVLink (tests/ipc_worker.py, directory bootstrap):
+    registered buffers read in place, torch.ops.nvrar across ranks, mixed
+    pinned/pageable host paths, delay injection and the word-atomicity canary
+    — every result bit-exact against the oracle."""
+    if NDEV < world:
+        pytest.skip(f"needs {world} GPUs, have {NDEV}")
+    import tempfile
+    with tempfile.TemporaryDirectory(prefix="nvrar_mg_") as d:
+        procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "ipc_worker.py"),
+                                   "--dir", d, "--rank", str(r), "--nodes", str(nodes),
+                                   "--gpus", str(gpus), "--device", str(r), "--quick",
+                                   "--registered", "--ops", "--host", "--jitter-seeds", "4",
+                                   "--canary", "20"],
+                                  stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                  cwd=ROOT) for r in range(world)]
+        outs = [p.communicate(timeout=600)[0] for p in procs]
+    text = "".join(outs)
+    assert all(p.returncode == 0 for p in procs), text[-4000:]
+    assert text.count(": OK") == world, text[-4000:]
