@@ -281,8 +281,10 @@ def run_emulated(args):
                      "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes": alg_bytes,
                      "note": "virtual ranks share one HBM: 2*P*M bytes (all inputs read, all "
-                             "outputs written) per launch; traffic = DRAM bytes of one launch "
-                             "of the chosen schedule's kernel from the committed ncu capture"},
+                             "outputs written) per launch; traffic = DRAM read + write bytes per "
+                             "launch of the chosen schedule's kernel in steady state (committed "
+                             "ncu capture over rotating buffers without cache flushes, so the "
+                             "write-back of earlier outputs is counted)"},
         "cpu_baseline": {"value": round(cpu_v, 3), "unit": "us", "cores": cpu_cores,
                          "kind": cpu_kind, "sample": cpu_sample},
         "e2e": {"value": round(statistics.median(e2e), 3), "unit": "us",
