@@ -145,7 +145,9 @@ struct LaunchParams {
 //   of the call — before it completes, so a mismatch still faults the call
 //   (sticky: later launches return at entry) — and a wait on a shorter peer's
 //   missing data is diagnosed as the length mismatch it is.
-enum : int { kFlagEarlySeq = 1, kFlagLazyLen = 2 };
+// kFlagL2Fetch256: the direct schedule's input loads carry the .L2::256B
+//   prefetch-size hint (set for pinned host inputs read over PCIe).
+enum : int { kFlagEarlySeq = 1, kFlagLazyLen = 2, kFlagL2Fetch256 = 4 };
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):
 //   NVRAR — ring fold of the node's ranks per G-chunk, pairwise tree over nodes;
@@ -195,6 +197,15 @@ __device__ __forceinline__ void st_mc16(void* p, uint32_t a, uint32_t b, uint32_
 __device__ __forceinline__ void st_volatile16(void* p, uint32_t a, uint32_t b, uint32_t c,
                                               uint32_t d) {
   asm volatile(NVRAR_PUT_ST " [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d));
+}
+
+// 16-byte read-only load with a 256-byte L2 fetch-size hint (aligned unit)
+__device__ __forceinline__ uint4 ld_l2_256(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
 }
 
 __device__ __forceinline__ uint64_t ld_volatile64(const void* p) {

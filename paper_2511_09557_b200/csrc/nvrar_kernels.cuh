@@ -868,6 +868,7 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   const uint32_t n_ord = lp.n_order ? static_cast<uint32_t>(lp.n_order) : n;
   const uint32_t SG = (n_ord + G - 1) / G;  // order in the whole vector's frame
   const uint32_t e_off = static_cast<uint32_t>(lp.e_off);
+  const bool l2pf = (lp.flags & kFlagL2Fetch256) != 0;
   const uint32_t U = (n + UE - 1) / UE;
   const uint32_t slice = (U + P - 1) / P;
   // small vectors leave the last ranks' slices empty (s0 clamps to U)
@@ -890,7 +891,19 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
 #pragma unroll
       for (int j = 0; j < MAXG; ++j) {
         if (j < G) {
-          load_raw<E, UE>(lp.send[nn * G + l], e0, valid, r[nn][j]);
+          const void* src = lp.send[nn * G + l];
+          const uint8_t* at = static_cast<const uint8_t*>(src) + static_cast<uint64_t>(e0) * E::kBytes;
+          if (l2pf && valid == UE && (reinterpret_cast<uintptr_t>(at) & 15u) == 0) {
+            // host (PCIe) inputs: ask the L2 for 256-byte fetches (fewer, larger
+            // read requests on the link)
+            const uint4 v = ld_l2_256(at);
+            r[nn][j][0] = v.x;
+            r[nn][j][1] = v.y;
+            r[nn][j][2] = v.z;
+            r[nn][j][3] = v.w;
+          } else {
+            load_raw<E, UE>(src, e0, valid, r[nn][j]);
+          }
           l = l + 1 == G ? 0 : l + 1;
         }
       }
