@@ -331,11 +331,20 @@ def run_multi(args, rank, world, local):
     # protocol), captured in the same graphs as NVRAR; torch.distributed's
     # all_reduce is kept as the framework-level reference
     from paper_2511_09557_b200 import nccl_ref
-    ncc = nccl_ref.Nccl(nccl_ref.lib_path("torch"))
-    uid = [ncc.unique_id() if rank == 0 else None]
+    ncc, nccl_version = None, None
+    try:
+        ncc = nccl_ref.Nccl(nccl_ref.lib_path("torch"))
+        uid = [ncc.unique_id() if rank == 0 else None]
+    except Exception:  # noqa: BLE001 — no loadable libnccl: torch.distributed's arm only
+        ncc, uid = None, [None]
     dist.broadcast_object_list(uid, src=0)
-    ncc.init_rank(world, uid[0], rank)
-    nccl_version = ncc.version()
+    ok = D.max_over_ranks([0.0 if (ncc is not None and uid[0] is not None) else 1.0],
+                          device=torch.device("cuda", local))[0] == 0.0
+    if ok:
+        ncc.init_rank(world, uid[0], rank)
+        nccl_version = ncc.version()
+    else:
+        ncc = None
 
     def measure(msg, impl, steps, warmup, producer=False):
         """p50-sorted per-call µs (max over ranks). producer: a cuBLAS GEMM writes
@@ -350,10 +359,11 @@ def run_multi(args, rank, world, local):
         if impl == "nvrar":
             plan = D.plan_consensus(comm.plan(ne, torch.bfloat16))
             fn = lambda i: comm.allreduce(bufs[i][0], bufs[i][1])  # noqa: E731
-        elif impl == "nccl":
+        elif impl == "nccl" and ncc is not None:
             plan = ("nccl-direct", 0)
             fn = lambda i: ncc.all_reduce(bufs[i][0], bufs[i][1])  # noqa: E731
         else:
+            impl = "torch"
             plan = ("torch.distributed", 0)
             fn = lambda i: dist.all_reduce(bufs[i][1])  # noqa: E731
             for a, b in bufs:
@@ -454,7 +464,8 @@ def run_multi(args, rank, world, local):
     # element count (the reference has fp32 / int32 only), rank 0 only
     cpu = cpu_reference(nodes, gpus, msg // 2, budget_s=10.0, max_calls=30) if rank == 0 else None
     traffic, traffic_src = profiled_nvlink_traffic(world, plan[0], msg)
-    ncc.close()
+    if ncc is not None:
+        ncc.close()
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(p50, 3), "unit": "us", "n_gpus": world,
@@ -480,8 +491,9 @@ def run_multi(args, rank, world, local):
                        "p10_us": round(per[len(per) // 10], 3),
                        "p90_us": round(per[(9 * len(per)) // 10], 3),
                        "nccl_p50_us": round(nccl50, 3),
-                       "nccl": f"ncclAllReduce direct (libnccl {nccl_version}, default "
-                               f"algorithm/protocol), same graph methodology",
+                       "nccl": (f"ncclAllReduce direct (libnccl {nccl_version}, default "
+                                f"algorithm/protocol), same graph methodology" if ncc is not None
+                                else "torch.distributed.all_reduce (direct libnccl unavailable)"),
                        "speedup_vs_nccl": round(nccl50 / p50, 3),
                        "torch_distributed_p50_us": round(torch50, 3),
                        "nccl_best": nccl_best.get(msg),
