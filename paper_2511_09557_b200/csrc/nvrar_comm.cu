@@ -1465,12 +1465,14 @@ int nvrar_mc_ready(nvrar_comm_t c, int* ready) {
 namespace {
 
 // Units per thread the direct schedule's grid is sized for when its buffers are
-// host memory read and written over PCIe (env NVRAR_HOST_UPT; default 8 —
-// measured N=1 e2e: 1 unit 321 us, 4 units 261 us, 8 units 246 us, 16 261 us).
+// host memory read and written over PCIe (env NVRAR_HOST_UPT; default 32 —
+// measured N=1 e2e, 2x4 x 1 MB fp32: 1 unit 321 us, 4 units 261 us, 8 units
+// 246-253 us, 16 248-257 us, 32 240-244 us: few long-running threads, each
+// streaming through a contiguous range, drive the PCIe link best).
 const int kHostUnitsPerThread = [] {
   const char* e = getenv("NVRAR_HOST_UPT");
-  const int v = e ? atoi(e) : 8;
-  return v >= 1 && v <= 64 ? v : 8;
+  const int v = e ? atoi(e) : 32;
+  return v >= 1 && v <= 64 ? v : 32;
 }();
 
 // Window of the host path (bytes per rank): nvrar_set_host_chunk or

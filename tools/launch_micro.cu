@@ -4,6 +4,11 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/launch_micro tools/launch_micro.cu
 //   ./tools/launch_micro
 #include <cuda_runtime.h>
+#include <cstdlib>
+
+#ifndef PAD_BYTES
+#define PAD_BYTES 8
+#endif
 
 #include <algorithm>
 #include <cstdint>
@@ -25,7 +30,10 @@ struct Args {
   uint64_t per_call_elems;  // uint4 per call
   int calls;
   unsigned* state;
-  int mode;  // bit0: pdl wait/trigger, bit1: state load+sync, bit2: copy
+  int mode;  // bit0: pdl wait/trigger, bit1: state load+sync, bit2: copy,
+             // bit3: state load as ld.relaxed.gpu (else ld.volatile = STRONG.SYS),
+             // bit4: state store right after the load (else at the end)
+  unsigned char pad[PAD_BYTES];  // parameter-block size experiment
 };
 
 __global__ void k_main(const __grid_constant__ Args a, int call) {
@@ -37,8 +45,13 @@ __global__ void k_main(const __grid_constant__ Args a, int call) {
   if (a.mode & 2) {
     if (threadIdx.x == 0) {
       unsigned v;
-      asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(a.state + blockIdx.x) : "memory");
+      if (a.mode & 8) {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.state + blockIdx.x) : "memory");
+      } else {
+        asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(a.state + blockIdx.x) : "memory");
+      }
       s = v;
+      if (a.mode & 16) a.state[blockIdx.x] = v + 1;
     }
     __syncthreads();
   }
@@ -51,12 +64,12 @@ __global__ void k_main(const __grid_constant__ Args a, int call) {
       a.out[base + i] = v;
     }
   }
-  if ((a.mode & 2) && threadIdx.x == 0) a.state[blockIdx.x] = s + 1;
+  if ((a.mode & 2) && !(a.mode & 16) && threadIdx.x == 0) a.state[blockIdx.x] = s + 1;
 }
 
 int run(const char* name, int mode, int grid, int block, bool pdl, uint64_t bytes, const uint4* in,
         uint4* out, unsigned* state, int ncalls_rot) {
-  Args a{in, out, bytes / 16, ncalls_rot, state, mode};
+  Args a{in, out, bytes / 16, ncalls_rot, state, mode, {}};
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   const int calls = 100;
@@ -112,6 +125,23 @@ int main() {
   CK(cudaMalloc(&state, 4096));
   CK(cudaMemset(in, 1, rot));
   CK(cudaMemset(state, 0, 4096));
+  if (getenv("LM_VARIANTS")) {
+    // round 2: where the fixed per-call cost of a state-reading kernel goes
+    printf("param block %d bytes\n", (int)sizeof(Args));
+    for (int grid : {64}) {
+      run("empty", 1, grid, 512, true, 0, in, out, state, 1);
+      run("state: volatile load + sync, store at end", 1 | 2, grid, 512, true, 0, in, out, state, 1);
+      run("state: relaxed.gpu load + sync, store at end", 1 | 2 | 8, grid, 512, true, 0, in, out, state, 1);
+      run("state: volatile load + sync, store early", 1 | 2 | 16, grid, 512, true, 0, in, out, state, 1);
+      run("state: relaxed.gpu load + sync, store early", 1 | 2 | 8 | 16, grid, 512, true, 0, in, out, state, 1);
+      const int rc = static_cast<int>(rot / (128ull << 10) / 2);
+      run("copy 128K", 1 | 4, grid, 512, true, 128ull << 10, in, out, state, rc);
+      run("state(volatile) + copy 128K", 1 | 2 | 4, grid, 512, true, 128ull << 10, in, out, state, rc);
+      run("state(relaxed.gpu, early store) + copy 128K", 1 | 2 | 4 | 8 | 16, grid, 512, true,
+          128ull << 10, in, out, state, rc);
+    }
+    return 0;
+  }
   for (int pdl = 0; pdl < 2; ++pdl) {
     for (int grid : {32, 128}) {
       run("empty", pdl ? 1 : 0, grid, 512, pdl, 0, in, out, state, 1);
