@@ -72,6 +72,9 @@ def worker(args) -> None:
                                                max(args.sizes), device=dev, timeout_s=30.0)
         if args.algo != "auto":
             comm.set_algo(args.algo)
+        if args.blocks:
+            from .comm import NvrarConfig
+            comm.set_config(NvrarConfig(args.blocks, 65536))
         if args.autotune:
             from .selector import autotune
             autotune(comm, sizes=args.sizes, dtype=torch.bfloat16, calls=30, reps=5)
@@ -164,6 +167,7 @@ def launch(args, extra_env=None) -> list:
     port = _port()
     procs = []
     wargs = ["worker", "--impl", args.impl, "--nodes", str(args.nodes), "--algo", args.algo,
+             "--blocks", str(args.blocks),
              "--sizes", ",".join(str(s) for s in args.sizes), "--steps", str(args.steps),
              "--warmup", str(args.warmup), "--calls", str(args.calls), "--producer",
              args.producer, "--nccl-lib", args.nccl_lib]
@@ -246,6 +250,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["nvrar", "nccl"], default="nvrar")
     ap.add_argument("--algo", default="auto")
     ap.add_argument("--autotune", action="store_true")
+    ap.add_argument("--blocks", type=int, default=0, help="CTAs per rank (0 = selector)")
     ap.add_argument("--sizes", default=",".join(str(s) for s in SIZES))
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
