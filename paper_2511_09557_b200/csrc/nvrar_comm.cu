@@ -384,7 +384,9 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_FAST_ONESHOT")) c->fast_oneshot = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_HOST_L2FETCH")) c->host_l2fetch = atoi(v) != 0;
-  if (const char* v = getenv("NVRAR_FLAGS")) c->flags = atoi(v) & (kFlagEarlySeq | kFlagLazyLen);
+  if (const char* v = getenv("NVRAR_FLAGS")) {
+    c->flags = atoi(v) & (kFlagEarlySeq | kFlagLazyLen | kFlagSeqBarrier);
+  }
   if (const char* v = getenv("NVRAR_THREADS")) {
     const int t = atoi(v);
     if (t >= 32 && t <= kThreads && t % 32 == 0) c->threads = t;

@@ -147,7 +147,9 @@ struct LaunchParams {
 //   missing data is diagnosed as the length mismatch it is.
 // kFlagL2Fetch256: the direct schedule's input loads carry the .L2::256B
 //   prefetch-size hint (set for pinned host inputs read over PCIe).
-enum : int { kFlagEarlySeq = 1, kFlagLazyLen = 2, kFlagL2Fetch256 = 4 };
+// kFlagSeqBarrier: thread 0 alone reads the call number and a __syncthreads
+//   broadcasts it (the round-1 prologue; default: every thread reads it).
+enum : int { kFlagEarlySeq = 1, kFlagLazyLen = 2, kFlagL2Fetch256 = 4, kFlagSeqBarrier = 8 };
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):
 //   NVRAR — ring fold of the node's ranks per G-chunk, pairwise tree over nodes;

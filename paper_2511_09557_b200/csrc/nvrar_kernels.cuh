@@ -86,14 +86,22 @@ __device__ __forceinline__ void begin_wait(const RankDesc& d) {
   stamp(d, 7);
 }
 
-// The call number and the sticky fault word of this CTA (thread 0 only). Only
-// this GPU's kernels write them (a gpu-scope load measured no faster).
+// The call number and the sticky fault word of this CTA. Only this GPU's
+// kernels write them (a gpu-scope load measured no faster). Every thread loads
+// them itself (the same two words per CTA: warp-broadcast loads), so no thread
+// waits at a barrier for thread 0's load — the barrier stalls dominated the
+// prologue (profiles/r02_summary.md §3). kFlagSeqBarrier (and kFlagEarlySeq,
+// whose early write-back must follow every warp's read) keep the round-1 form:
+// thread 0 loads, a __syncthreads broadcasts.
 struct SeqWords {
   uint32_t err, seq;
 };
-__device__ __forceinline__ SeqWords seq_issue(const RankDesc& d) {
+__device__ __forceinline__ bool seq_per_thread(int flags) {
+  return (flags & (kFlagSeqBarrier | kFlagEarlySeq)) == 0;
+}
+__device__ __forceinline__ SeqWords seq_issue(const RankDesc& d, int flags = 0) {
   SeqWords w{0u, 0u};
-  if (threadIdx.x == 0) {
+  if (seq_per_thread(flags) || threadIdx.x == 0) {
     w.err = ld_volatile32(&d.state->err.code);
     w.seq = ld_volatile32(&d.state->seq[blockIdx.x]);
   }
@@ -102,13 +110,17 @@ __device__ __forceinline__ SeqWords seq_issue(const RankDesc& d) {
 
 // Prologue, part 2 (after the caller has issued its first input loads, which
 // do not depend on the call number). Returns false on a sticky fault.
-__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, SeqWords w) {
-  __shared__ uint32_t s_seq, s_err;
-  if (threadIdx.x == 0) {
-    s_err = w.err;
-    s_seq = w.seq;
+__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, SeqWords w, int flags = 0) {
+  if (!seq_per_thread(flags)) {
+    __shared__ uint32_t s_seq, s_err;
+    if (threadIdx.x == 0) {
+      s_err = w.err;
+      s_seq = w.seq;
+    }
+    __syncthreads();
+    w.err = s_err;
+    w.seq = s_seq;
   }
-  __syncthreads();
   c.st = d.state;
   c.timeout_ns = d.timeout_ns;
   c.poll_ns = d.poll_ns;
@@ -120,16 +132,18 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, SeqWords w)
   c.len_words = nullptr;
   c.len = 0;
   c.t0 = globaltimer();
-  c.seq = s_seq + 1u;
+  c.seq = w.seq + 1u;
   c.phase = 2;
   stamp(d, 1);
-  return s_err == 0u;
+  return w.err == 0u;
 }
-__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c) {
-  return begin_seq(d, c, seq_issue(d));
+__device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, int flags = 0) {
+  return begin_seq(d, c, seq_issue(d, flags), flags);
 }
 
 __device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
+  // every warp of the CTA has read slot b (seq_issue) before it is rewritten
+  __syncthreads();
   // CTA b owns slots b, b + grid, ...; warp 0 writes them (small grids own many)
   if (threadIdx.x < 32) {
     for (int i = blockIdx.x + static_cast<int>(threadIdx.x) * gridDim.x; i < kSeqSlots;
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   for (int j = 0; j < MG; ++j) grp[j] = local + j >= G ? local + j - G : local + j;
 
   begin_wait(d);
-  const SeqWords sw = seq_issue(d);
+  const SeqWords sw = seq_issue(d, lp.flags);
   // Prefetch this thread's first unit of every chunk while the call number is
   // read (the loads do not depend on it): pre[j] = chunk (local + j) % G.
   uint32_t pre[MG][RDW];
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
   }
   Ctl c;
-  if (!begin_seq(d, c, sw)) return;  // sticky fault: comm is dead
+  if (!begin_seq(d, c, sw, lp.flags)) return;  // sticky fault: comm is dead
   const uint32_t parity = c.seq & 1u;
   if (lp.flags & kFlagEarlySeq) end_call(d, c.seq);
 
@@ -560,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 
   begin_wait(d);
   // the call-number load first: its latency overlaps the input prefetch
-  const SeqWords sw = seq_issue(d);
+  const SeqWords sw = seq_issue(d, lp.flags);
   // Prefetch this thread's first unit of every sub-shard (pre[j]: owner
   // (me + j) % P; j = 0 is our own) before the call number is read. One-shot
   // sends the same unit to everyone, so it loads once.
@@ -577,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
   }
   Ctl c;
-  if (!begin_seq(d, c, sw)) return;
+  if (!begin_seq(d, c, sw, lp.flags)) return;
   const uint32_t parity = c.seq & 1u;
   const bool lazy_len = !EMU && (lp.flags & kFlagLazyLen) != 0;
   if (lp.flags & kFlagEarlySeq) end_call(d, c.seq);
@@ -1003,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, 1) pull_kernel(const __grid_constant
   const RankDesc& d = lp.d0;
   begin_wait(d);
   Ctl c;
-  if (!begin_seq(d, c)) return;
+  if (!begin_seq(d, c, lp.flags)) return;
   const int P = d.world, me = d.rank, G = d.gpus;
   const uint32_t n = static_cast<uint32_t>(lp.count);
   const uint32_t SG = (n + G - 1) / G;
