@@ -161,6 +161,13 @@ enum : int { kOrderNvrar = 0, kOrderRing = 1, kOrderTree = 2 };
 // ---------------------------------------------------------------------------
 // PTX primitives
 
+// Branch-layout hints: the hot path of a call (aligned full units, no residual,
+// no injected delay, no fault) is laid out contiguously, the rare cases out of
+// the way — the instruction fetch at the start of every call is part of the
+// small-message latency (profiles/r02_summary.md §3).
+#define NVRAR_LIKELY(x) __builtin_expect(!!(x), 1)
+#define NVRAR_UNLIKELY(x) __builtin_expect(!!(x), 0)
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -303,8 +310,8 @@ static __device__ __noinline__ int wait_check(RankState* st, uint64_t t0, uint64
 // Called while a wait is unsatisfied. Returns true when the thread must give up.
 __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t word,
                                           uint64_t observed) {
-  if (c.aborted) return true;
-  if ((++c.spins & 127u) != 0u) return false;
+  if (NVRAR_UNLIKELY(c.aborted)) return true;
+  if (NVRAR_LIKELY((++c.spins & 127u) != 0u)) return false;
   const int r = wait_check(c.st, c.t0, c.timeout_ns, c.last_chance ? 1 : 0, c.len_words, c.len,
                            c.spins, c.seq, c.phase, kind, peer, word, observed);
   if (r == 1) {
@@ -337,7 +344,7 @@ static __device__ __noinline__ void jitter_sleep(uint32_t seed, uint32_t key, ui
 
 __device__ __forceinline__ void poll_pause(const Ctl& c) {
   __nanosleep(c.poll_ns ? c.poll_ns : 32u);
-  if (c.jitter_ns) {
+  if (NVRAR_UNLIKELY(c.jitter_ns != 0)) {
     jitter_sleep(c.jitter_seed, c.spins * 0x9E3779B9u ^ threadIdx.x ^ (blockIdx.x << 16),
                  c.jitter_ns);
   }
@@ -346,7 +353,7 @@ __device__ __forceinline__ void poll_pause(const Ctl& c) {
 // Injected delay at a program point (`site`) of call `seq`: the same for a
 // whole warp (per CTA, warp, unit group and site), different per seed.
 __device__ __forceinline__ void jitter(const Ctl& c, uint32_t site) {
-  if (c.jitter_ns == 0) return;
+  if (NVRAR_LIKELY(c.jitter_ns == 0)) return;
   jitter_sleep(c.jitter_seed,
                c.seq * 0x9E3779B9u ^ (blockIdx.x << 20) ^ (blockIdx.y << 26) ^
                    ((threadIdx.x >> 5) << 8) ^ site,
@@ -675,7 +682,7 @@ __device__ __forceinline__ void load_raw(const void* p, uint64_t e, int valid,
   constexpr int RDW = UE * E::kBytes / 4;
   if constexpr (E::kBytes == 4) {
     const uint32_t* q = static_cast<const uint32_t*>(p) + e;
-    if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+    if (NVRAR_LIKELY(valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0)) {
 #pragma unroll
       for (int h = 0; h < RDW / 4; ++h) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(q) + h);
@@ -691,7 +698,7 @@ __device__ __forceinline__ void load_raw(const void* p, uint64_t e, int valid,
   } else {
     const uint16_t* q = static_cast<const uint16_t*>(p) + e;
     if constexpr (RDW == 4) {
-      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+      if (NVRAR_LIKELY(valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0)) {
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(q));
         d[0] = v.x;
         d[1] = v.y;
@@ -700,7 +707,7 @@ __device__ __forceinline__ void load_raw(const void* p, uint64_t e, int valid,
         return;
       }
     } else {
-      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 7u) == 0) {
+      if (NVRAR_LIKELY(valid == UE && (reinterpret_cast<uintptr_t>(q) & 7u) == 0)) {
         const uint2 v = __ldg(reinterpret_cast<const uint2*>(q));
         d[0] = v.x;
         d[1] = v.y;
@@ -722,7 +729,7 @@ __device__ __forceinline__ void store_raw(void* p, uint64_t e, int valid,
   constexpr int RDW = UE * E::kBytes / 4;
   if constexpr (E::kBytes == 4) {
     uint32_t* q = static_cast<uint32_t*>(p) + e;
-    if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+    if (NVRAR_LIKELY(valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0)) {
 #pragma unroll
       for (int h = 0; h < RDW / 4; ++h) {
         reinterpret_cast<uint4*>(q)[h] = make_uint4(d[4 * h], d[4 * h + 1], d[4 * h + 2], d[4 * h + 3]);
@@ -735,12 +742,12 @@ __device__ __forceinline__ void store_raw(void* p, uint64_t e, int valid,
   } else {
     uint16_t* q = static_cast<uint16_t*>(p) + e;
     if constexpr (RDW == 4) {
-      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+      if (NVRAR_LIKELY(valid == UE && (reinterpret_cast<uintptr_t>(q) & 15u) == 0)) {
         *reinterpret_cast<uint4*>(q) = make_uint4(d[0], d[1], d[2], d[3]);
         return;
       }
     } else {
-      if (valid == UE && (reinterpret_cast<uintptr_t>(q) & 7u) == 0) {
+      if (NVRAR_LIKELY(valid == UE && (reinterpret_cast<uintptr_t>(q) & 7u) == 0)) {
         *reinterpret_cast<uint2*>(q) = make_uint2(d[0], d[1]);
         return;
       }
@@ -803,7 +810,7 @@ __device__ __forceinline__ void stamp(const RankDesc& d, int k) {
 // in flight (no registers held; emit's load then hits L2).
 template <class E>
 __device__ __forceinline__ void prefetch_resid(const void* resid, uint64_t e) {
-  if (resid != nullptr) {
+  if (NVRAR_UNLIKELY(resid != nullptr)) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(resid) + e * E::kBytes));
   }
 }
@@ -812,7 +819,7 @@ __device__ __forceinline__ void prefetch_resid(const void* resid, uint64_t e) {
 template <class E, int UE>
 __device__ __forceinline__ void emit(void* recv, const void* resid, uint64_t e, int valid,
                                      const uint32_t (&o)[UE * E::kBytes / 4]) {
-  if (resid == nullptr) {
+  if (NVRAR_LIKELY(resid == nullptr)) {
     store_raw<E, UE>(recv, e, valid, o);
     return;
   }

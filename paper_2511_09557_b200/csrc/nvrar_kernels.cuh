@@ -558,15 +558,21 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const int order = SHOT == 1 ? static_cast<int>(kOrderNvrar) : lp.order;
   // members of one fold: the node's G ranks, or (ring order) all P ranks
   const int OG = order == kOrderRing ? P : G;
-  const uint64_t n_ord = lp.n_order ? lp.n_order : n;  // order follows the whole vector
-  const uint64_t SG = (n_ord + OG - 1) / OG;
+  // 32-bit index math: the host rejects vectors of 2^31 or more elements
+  // (64-bit divisions compile to an out-of-line routine on the prologue path)
+  const uint32_t n_ord = static_cast<uint32_t>(lp.n_order ? lp.n_order : n);  // the whole vector
+  const uint32_t SG = (n_ord + static_cast<uint32_t>(OG) - 1u) / static_cast<uint32_t>(OG);
   const uint32_t e_off = static_cast<uint32_t>(lp.e_off);
-  constexpr uint64_t kAlign = UE;
-  const uint64_t SP = oneshot ? ((n + kAlign - 1) / kAlign) * kAlign
-                              : ((((n + P - 1) / P) + kAlign - 1) / kAlign) * kAlign;
-  const uint64_t U = SP / UE;
-  const uint64_t ub = U * blockIdx.x / gridDim.x;
-  const uint64_t ue = U * (blockIdx.x + 1) / gridDim.x;
+  constexpr uint32_t kAlign = UE;
+  const uint32_t n32a = static_cast<uint32_t>(n);
+  const uint32_t SP = oneshot ? ((n32a + kAlign - 1u) / kAlign) * kAlign
+                              : ((((n32a + static_cast<uint32_t>(P) - 1u) / static_cast<uint32_t>(P)) +
+                                  kAlign - 1u) / kAlign) * kAlign;
+  const uint32_t U = SP / UE;
+  // this CTA's units: an even split, the first U % grid CTAs one more
+  const uint32_t uq = U / gridDim.x, ur = U % gridDim.x;
+  const uint64_t ub = static_cast<uint64_t>(uq) * blockIdx.x + (blockIdx.x < ur ? blockIdx.x : ur);
+  const uint64_t ue = ub + uq + (blockIdx.x < ur ? 1u : 0u);
   const void* send = EMU ? lp.send[blockIdx.y] : lp.send[0];
   void* recv = EMU ? lp.recv[blockIdx.y] : lp.recv[0];
   const void* resid = EMU ? lp.resid[blockIdx.y] : lp.resid[0];
@@ -697,8 +703,8 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     const uint32_t eg0 = e0 + e_off;  // index in the whole vector (the order's frame)
     // the tree chain does not depend on the chunk: one fixed order
     const int c0 = tree ? 0 : static_cast<int>(eg0 / SG32);
-    const bool straddle =
-        !tree && eg0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32;
+    const bool straddle = NVRAR_UNLIKELY(
+        !tree && eg0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32);
     int l0 = tree ? OG - 1 : c0 + 1;
     if (l0 >= OG) l0 -= OG;
 
@@ -744,7 +750,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 #pragma unroll
     for (int nn = 0; nn < N; ++nn) {
       A v[UE];
-      if (c0 == c3) {
+      if (NVRAR_LIKELY(c0 == c3)) {
         raw_to_acc<UE>(E{}, r[nn][0], v);
 #pragma unroll
         for (int j = 1; j < MAXG; ++j) {
