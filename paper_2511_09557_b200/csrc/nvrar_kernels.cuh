@@ -101,6 +101,9 @@ __device__ __forceinline__ bool seq_per_thread(int flags) {
 }
 __device__ __forceinline__ SeqWords seq_issue(const RankDesc& d, int flags = 0) {
   SeqWords w{0u, 0u};
+#ifdef NVRAR_ABL_NO_SEQ  // experiment builds only (tools/ablate.sh): no call-number read
+  return w;
+#endif
   if (seq_per_thread(flags) || threadIdx.x == 0) {
     w.err = ld_volatile32(&d.state->err.code);
     w.seq = ld_volatile32(&d.state->seq[blockIdx.x]);
@@ -142,6 +145,9 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, int flags =
 }
 
 __device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
+#ifdef NVRAR_ABL_NO_END  // experiment builds only (tools/ablate.sh): no counter write-back
+  return;
+#endif
   // every warp of the CTA has read slot b (seq_issue) before it is rewritten
   __syncthreads();
   // CTA b owns slots b, b + grid, ...; warp 0 writes them (small grids own many)
@@ -680,7 +686,9 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       if (p != me) wait_seq_len(c, d, p, n);
     }
+#ifndef NVRAR_ABL_NO_SYNC2  // experiment builds only (tools/ablate.sh)
     __syncthreads();
+#endif
   }
   stamp(d, 3);
   c.phase = 4;
