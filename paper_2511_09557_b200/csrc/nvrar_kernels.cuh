@@ -905,6 +905,17 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   const uint32_t ub = s0 + static_cast<uint32_t>(static_cast<uint64_t>(s1 - s0) * blockIdx.x / gridDim.x);
   const uint32_t ue = s0 + static_cast<uint32_t>(static_cast<uint64_t>(s1 - s0) * (blockIdx.x + 1) / gridDim.x);
 
+  // Nothing here waits on a peer, so the call number is never needed: advance
+  // this CTA's replicated counter slots by one without reading them (a sticky
+  // fault cannot arise in this schedule; the host refuses a failed comm). Done
+  // first, so the atomics complete while the loads are in flight instead of
+  // on the kernel's tail (the next call reads the slots after this grid).
+  if (threadIdx.x < 32) {
+    for (int i = blockIdx.x + static_cast<int>(threadIdx.x) * gridDim.x; i < kSeqSlots;
+         i += 32 * gridDim.x) {
+      atomicAdd(&st->seq[i], 1u);
+    }
+  }
   uint32_t r[N][MAXG][RDW];
   // loads of unit u from every rank, in each node's fold order (starting at the
   // chunk after the unit's own, ring.hpp fold order)
@@ -996,15 +1007,6 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
     u += blockDim.x;
     if (u < ue) load_unit(u);
     for (int r2 = 0; r2 < P; ++r2) emit<E, UE>(lp.recv[r2], lp.resid[r2], e0, valid, o);
-  }
-  // Nothing here waits on a peer, so the call number is never needed: advance
-  // this CTA's replicated counter slots by one without reading them (a sticky
-  // fault cannot arise in this schedule; the host refuses a failed comm).
-  if (threadIdx.x < 32) {
-    for (int i = blockIdx.x + static_cast<int>(threadIdx.x) * gridDim.x; i < kSeqSlots;
-         i += 32 * gridDim.x) {
-      atomicAdd(&st->seq[i], 1u);
-    }
   }
   stamp(d, 6);
 }
