@@ -144,19 +144,24 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, int flags =
   return begin_seq(d, c, seq_issue(d, flags), flags);
 }
 
-__device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
+// CTA b owns slots b, b + grid, ...; warp 0 writes them (small grids own many).
+// The caller guarantees every warp of the CTA has read slot b already.
+__device__ __forceinline__ void write_seq_slots(const RankDesc& d, uint32_t seq) {
 #ifdef NVRAR_ABL_NO_END  // experiment builds only (tools/ablate.sh): no counter write-back
   return;
 #endif
-  // every warp of the CTA has read slot b (seq_issue) before it is rewritten
-  __syncthreads();
-  // CTA b owns slots b, b + grid, ...; warp 0 writes them (small grids own many)
   if (threadIdx.x < 32) {
     for (int i = blockIdx.x + static_cast<int>(threadIdx.x) * gridDim.x; i < kSeqSlots;
          i += 32 * gridDim.x) {
       d.state->seq[i] = seq;
     }
   }
+}
+
+__device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
+  // every warp of the CTA has read slot b (seq_issue) before it is rewritten
+  __syncthreads();
+  write_seq_slots(d, seq);
   stamp(d, 6);
 }
 
@@ -682,6 +687,13 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   stamp(d, 2);
   c.phase = 3;
 
+  // the counter write-back rides on this barrier when there is one: every warp
+  // has read the call number before it, and the stores leave the kernel's tail
+#ifdef NVRAR_ABL_NO_SYNC2
+  const bool seq_mid = false;
+#else
+  const bool seq_mid = !lazy_len && !(lp.flags & kFlagEarlySeq);
+#endif
   if (!lazy_len) {
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       if (p != me) wait_seq_len(c, d, p, n);
@@ -689,6 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 #ifndef NVRAR_ABL_NO_SYNC2  // experiment builds only (tools/ablate.sh)
     __syncthreads();
 #endif
+    if (seq_mid) write_seq_slots(d, c.seq);
   }
   stamp(d, 3);
   c.phase = 4;
@@ -872,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
   }
   stamp(d, 5);
-  if (!(lp.flags & kFlagEarlySeq)) end_call(d, c.seq);
+  if (!(lp.flags & kFlagEarlySeq) && !seq_mid) end_call(d, c.seq);
 }
 
 // ---------------------------------------------------------------------------
