@@ -105,6 +105,7 @@ struct nvrar_comm {
   int flags = 0;  // LaunchParams.flags (schedule variants; NVRAR_FLAGS)
   bool fast_oneshot = true;  // one-shot calls run the specialised kernel (SHOT = 1)
   bool host_l2fetch = true;  // 256-byte L2 fetches for host inputs (NVRAR_HOST_L2FETCH=0: off)
+  bool dev_l2fetch = false;  // the same hint on device inputs (NVRAR_DEV_L2FETCH=1; experiment)
   int threads = kThreads;  // threads per CTA (multiple of 32, <= kThreads)
   uint64_t pp_base[kMaxRanks] = {};  // per-peer ping-pong counter (same on both sides)
   uint32_t canary_base[kMaxRanks] = {};  // per-peer canary flag base (same on both sides)
@@ -384,6 +385,7 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   if (const char* v = getenv("NVRAR_PDL")) c->pdl = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_FAST_ONESHOT")) c->fast_oneshot = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_HOST_L2FETCH")) c->host_l2fetch = atoi(v) != 0;
+  if (const char* v = getenv("NVRAR_DEV_L2FETCH")) c->dev_l2fetch = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_FLAGS")) {
     c->flags = atoi(v) & (kFlagEarlySeq | kFlagLazyLen | kFlagSeqBarrier);
   }
@@ -961,6 +963,7 @@ static int launch(nvrar_comm_t* comms, int ncomms, const void* const* send, void
   lp.n_order = n_order;
   lp.flags = c0->flags;
   if (upt > 1 && c0->host_l2fetch) lp.flags |= kFlagL2Fetch256;  // host buffers over PCIe
+  if (upt <= 1 && c0->dev_l2fetch) lp.flags |= kFlagL2Fetch256;   // experiment: device inputs
   CUDA_TRY(c0, cudaSetDevice(c0->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (count == 0) {
