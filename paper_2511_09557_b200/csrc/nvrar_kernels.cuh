@@ -715,9 +715,22 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
                           static_cast<uint64_t>(parity) * d.world * d.lay.a_src * 8;
   const uint64_t a_stride = d.lay.a_src * 8;
   uint64_t len_seen = 0;
+  // this rank's own unit of the NEXT iteration is loaded one iteration ahead,
+  // so a thread with several units does not wait for an HBM load per unit
+  uint32_t own_next[RDW];
+#pragma unroll
+  for (int q = 0; q < RDW; ++q) own_next[q] = pre[0][q];
   for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
     const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
+    uint32_t own[RDW];
+#pragma unroll
+    for (int q = 0; q < RDW; ++q) own[q] = own_next[q];
+    if (u + blockDim.x < ue) {
+      const uint32_t e1 = e0 + UE * blockDim.x;
+      const int v1 = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e1));
+      if (v1 > 0) load_raw<E, UE>(send, e1, v1, own_next);
+    }
     if (valid == 0) continue;
     prefetch_resid<E>(resid, e0);
     const bool tree = order == kOrderTree;
@@ -745,11 +758,9 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         slots[nn][j] = reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(src[nn][j]) * a_stride);
         if (j < OG) {
           const int s = src[nn][j];
-          if (s == me && u == u_first) {
+          if (s == me) {
 #pragma unroll
-            for (int q = 0; q < RDW; ++q) r[nn][j][q] = pre[0][q];
-          } else if (s == me) {
-            load_raw<E, UE>(send, e0, valid, r[nn][j]);
+            for (int q = 0; q < RDW; ++q) r[nn][j][q] = own[q];
           } else {
             pending |= 1u << (nn * MAXG + j);
           }
