@@ -259,9 +259,11 @@ struct Ctl {
 // and inlined at every poll site they made the kernels several times larger —
 // the hot path then spread over more instruction-cache lines (no_instruction
 // stalls dominated the one-shot's profile, profiles/r02_ncu_nvlink_p2.json).
-static __device__ __noinline__ void record_fault_at(RankState* st, uint32_t code, int kind, int peer,
-                                             uint32_t seq, uint64_t word, uint64_t observed,
-                                             int phase) {
+// Poll sites holding a large register tile (16 sources) keep them inline
+// (kOutline = false): a call there makes the caller save the tile.
+__device__ __forceinline__ void record_fault_body(RankState* st, uint32_t code, int kind, int peer,
+                                                  uint32_t seq, uint64_t word, uint64_t observed,
+                                                  int phase) {
   ErrRec* e = &st->err;
   if (atomicCAS(&e->code, 0u, 0xFFFFFFFFu) == 0u) {
     e->kind = kind;
@@ -275,10 +277,20 @@ static __device__ __noinline__ void record_fault_at(RankState* st, uint32_t code
     atomicExch(&e->code, code);
   }
 }
+static __device__ __noinline__ void record_fault_at(RankState* st, uint32_t code, int kind,
+                                                    int peer, uint32_t seq, uint64_t word,
+                                                    uint64_t observed, int phase) {
+  record_fault_body(st, code, kind, peer, seq, word, observed, phase);
+}
 
+template <bool kOutline = true>
 __device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, int peer,
                                              uint64_t word, uint64_t observed) {
-  record_fault_at(c.st, code, kind, peer, c.seq, word, observed, c.phase);
+  if constexpr (kOutline) {
+    record_fault_at(c.st, code, kind, peer, c.seq, word, observed, c.phase);
+  } else {
+    record_fault_body(c.st, code, kind, peer, c.seq, word, observed, c.phase);
+  }
   c.aborted = true;
 }
 
@@ -286,34 +298,50 @@ __device__ __forceinline__ void record_fault(Ctl& c, uint32_t code, int kind, in
 // recorded, here or by another thread), 2 = the deadline passed once (poll one
 // more full round before declaring a deadlock: a thread can be descheduled
 // between its poll and this check).
-static __device__ __noinline__ int wait_check(RankState* st, uint64_t t0, uint64_t timeout_ns,
-                                       int last_chance, const uint64_t* len_words, uint32_t len,
-                                       uint32_t spins, uint32_t seq, int phase, int kind, int peer,
-                                       uint64_t word, uint64_t observed) {
+__device__ __forceinline__ int wait_check_body(RankState* st, uint64_t t0, uint64_t timeout_ns,
+                                               int last_chance, const uint64_t* len_words,
+                                               uint32_t len, uint32_t spins, uint32_t seq,
+                                               int phase, int kind, int peer, uint64_t word,
+                                               uint64_t observed) {
   if (ld_volatile32(&st->err.code) != 0u) return 1;
   if (len_words != nullptr && kind == kFlagWait && peer >= 0 && (spins & 4095u) == 0u) {
     // a data wait that lasts: is the peer in this call with another length?
     const uint64_t v = ld_volatile64(len_words + peer);
     if (static_cast<uint32_t>(v >> 32) == seq && static_cast<uint32_t>(v) != len) {
-      record_fault_at(st, kProtocolFault, kLenMismatch, peer, seq, 0, v, phase);
+      record_fault_body(st, kProtocolFault, kLenMismatch, peer, seq, 0, v, phase);
       return 1;
     }
   }
   if (globaltimer() - t0 > timeout_ns) {
     if (!last_chance) return 2;
-    record_fault_at(st, kDeadlock, kind, peer, seq, word, observed, phase);
+    record_fault_body(st, kDeadlock, kind, peer, seq, word, observed, phase);
     return 1;
   }
   return 0;
 }
+static __device__ __noinline__ int wait_check(RankState* st, uint64_t t0, uint64_t timeout_ns,
+                                              int last_chance, const uint64_t* len_words,
+                                              uint32_t len, uint32_t spins, uint32_t seq,
+                                              int phase, int kind, int peer, uint64_t word,
+                                              uint64_t observed) {
+  return wait_check_body(st, t0, timeout_ns, last_chance, len_words, len, spins, seq, phase, kind,
+                         peer, word, observed);
+}
 
 // Called while a wait is unsatisfied. Returns true when the thread must give up.
+template <bool kOutline = true>
 __device__ __forceinline__ bool wait_tick(Ctl& c, int kind, int peer, uint64_t word,
                                           uint64_t observed) {
   if (NVRAR_UNLIKELY(c.aborted)) return true;
   if (NVRAR_LIKELY((++c.spins & 127u) != 0u)) return false;
-  const int r = wait_check(c.st, c.t0, c.timeout_ns, c.last_chance ? 1 : 0, c.len_words, c.len,
-                           c.spins, c.seq, c.phase, kind, peer, word, observed);
+  int r;
+  if constexpr (kOutline) {
+    r = wait_check(c.st, c.t0, c.timeout_ns, c.last_chance ? 1 : 0, c.len_words, c.len, c.spins,
+                   c.seq, c.phase, kind, peer, word, observed);
+  } else {
+    r = wait_check_body(c.st, c.t0, c.timeout_ns, c.last_chance ? 1 : 0, c.len_words, c.len,
+                        c.spins, c.seq, c.phase, kind, peer, word, observed);
+  }
   if (r == 1) {
     c.aborted = true;
     return true;
@@ -342,11 +370,16 @@ static __device__ __noinline__ void jitter_sleep(uint32_t seed, uint32_t key, ui
   __nanosleep(mix32(seed ^ mix32(key)) % max_ns);
 }
 
+template <bool kOutline = true>
 __device__ __forceinline__ void poll_pause(const Ctl& c) {
   __nanosleep(c.poll_ns ? c.poll_ns : 32u);
   if (NVRAR_UNLIKELY(c.jitter_ns != 0)) {
-    jitter_sleep(c.jitter_seed, c.spins * 0x9E3779B9u ^ threadIdx.x ^ (blockIdx.x << 16),
-                 c.jitter_ns);
+    const uint32_t key = c.spins * 0x9E3779B9u ^ threadIdx.x ^ (blockIdx.x << 16);
+    if constexpr (kOutline) {
+      jitter_sleep(c.jitter_seed, key, c.jitter_ns);
+    } else {
+      __nanosleep(mix32(c.jitter_seed ^ mix32(key)) % c.jitter_ns);
+    }
   }
 }
 
@@ -527,7 +560,7 @@ __device__ __forceinline__ void recv_all(Ctl& c, uint4* const (&slot)[K], const 
           Pr::template clear<W>(slot[k], u[k]);
           pending &= ~(1u << k);
         } else if (!Pr::kLamport && flag_ahead(bad, c.seq)) {
-          record_fault(c, kProtocolFault, kStaleFlag, peer[k], u[k], bad);
+          record_fault<(K <= 8)>(c, kProtocolFault, kStaleFlag, peer[k], u[k], bad);
           return;
         }
       }
@@ -543,8 +576,8 @@ __device__ __forceinline__ void recv_all(Ctl& c, uint4* const (&slot)[K], const 
           uk = u[k];
         }
       }
-      if (wait_tick(c, kFlagWait, pk, uk, bad)) return;
-      poll_pause(c);
+      if (wait_tick<(K <= 8)>(c, kFlagWait, pk, uk, bad)) return;
+      poll_pause<(K <= 8)>(c);
     }
   }
 }
@@ -566,7 +599,7 @@ __device__ __forceinline__ void recv_grid(Ctl& c, uint4* const (&slot)[NN][MM], 
             Pr::template clear<W>(slot[a][m], u);
             pending &= ~bit;
           } else if (!Pr::kLamport && flag_ahead(bad, c.seq)) {
-            record_fault(c, kProtocolFault, kStaleFlag, peer[a][m], u, bad);
+            record_fault<(NN * MM <= 8)>(c, kProtocolFault, kStaleFlag, peer[a][m], u, bad);
             return;
           }
         }
@@ -582,8 +615,52 @@ __device__ __forceinline__ void recv_grid(Ctl& c, uint4* const (&slot)[NN][MM], 
           if (a * MM + m == k0) pk = peer[a][m];
         }
       }
-      if (wait_tick(c, kFlagWait, pk, u, bad)) return;
-      poll_pause(c);
+      if (wait_tick<(NN * MM <= 8)>(c, kFlagWait, pk, u, bad)) return;
+      poll_pause<(NN * MM <= 8)>(c);
+    }
+  }
+}
+
+// Same, for NN rows of MM source cells where row a is unit u[a] (bit a*MM + m).
+template <class Pr, int W, int NN, int MM>
+__device__ __forceinline__ void recv_rows(Ctl& c, uint4* const (&slot)[NN][MM],
+                                          const uint64_t (&u)[NN], uint32_t (&d)[NN][MM][W],
+                                          uint32_t pending, const int (&peer)[NN][MM]) {
+  constexpr bool kOutline = NN * MM <= 8;
+  while (pending) {
+    uint32_t bad = 0;
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const uint32_t bit = 1u << (a * MM + m);
+        if (pending & bit) {
+          if (Pr::template try_get<W>(slot[a][m], u[a], c.seq, d[a][m], bad)) {
+            Pr::template clear<W>(slot[a][m], u[a]);
+            pending &= ~bit;
+          } else if (!Pr::kLamport && flag_ahead(bad, c.seq)) {
+            record_fault<kOutline>(c, kProtocolFault, kStaleFlag, peer[a][m], u[a], bad);
+            return;
+          }
+        }
+      }
+    }
+    if (pending) {
+      const int k0 = __ffs(pending) - 1;
+      int pk = 0;
+      uint64_t uk = 0;
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+          if (a * MM + m == k0) {
+            pk = peer[a][m];
+            uk = u[a];
+          }
+        }
+      }
+      if (wait_tick<kOutline>(c, kFlagWait, pk, uk, bad)) return;
+      poll_pause<kOutline>(c);
     }
   }
 }

@@ -717,6 +717,8 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   uint64_t len_seen = 0;
   // this rank's own unit of the NEXT iteration is loaded one iteration ahead,
   // so a thread with several units does not wait for an HBM load per unit
+  // (small tiles only: with 16 sources the extra live registers spill)
+  constexpr bool kOwnAhead = N * MAXG <= 8;
   uint32_t own_next[RDW];
 #pragma unroll
   for (int q = 0; q < RDW; ++q) own_next[q] = pre[0][q];
@@ -724,12 +726,14 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);
     const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
     uint32_t own[RDW];
+    if constexpr (kOwnAhead) {
 #pragma unroll
-    for (int q = 0; q < RDW; ++q) own[q] = own_next[q];
-    if (u + blockDim.x < ue) {
-      const uint32_t e1 = e0 + UE * blockDim.x;
-      const int v1 = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e1));
-      if (v1 > 0) load_raw<E, UE>(send, e1, v1, own_next);
+      for (int q = 0; q < RDW; ++q) own[q] = own_next[q];
+      if (u + blockDim.x < ue) {
+        const uint32_t e1 = e0 + UE * blockDim.x;
+        const int v1 = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e1));
+        if (v1 > 0) load_raw<E, UE>(send, e1, v1, own_next);
+      }
     }
     if (valid == 0) continue;
     prefetch_resid<E>(resid, e0);
@@ -759,8 +763,15 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
         if (j < OG) {
           const int s = src[nn][j];
           if (s == me) {
+            if constexpr (kOwnAhead) {
 #pragma unroll
-            for (int q = 0; q < RDW; ++q) r[nn][j][q] = own[q];
+              for (int q = 0; q < RDW; ++q) r[nn][j][q] = own[q];
+            } else if (u == u_first) {
+#pragma unroll
+              for (int q = 0; q < RDW; ++q) r[nn][j][q] = pre[0][q];
+            } else {
+              load_raw<E, UE>(send, e0, valid, r[nn][j]);
+            }
           } else {
             pending |= 1u << (nn * MAXG + j);
           }
@@ -842,38 +853,50 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   if (!oneshot) {
     uint8_t* const b_mine = d.base[me] + d.lay.b_off + static_cast<uint64_t>(parity) * d.world * d.lay.b_src * 8;
     const uint64_t b_stride = d.lay.b_src * 8;
-    constexpr int kGrp = 8;  // sources polled together (P <= 8: one group)
-    for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
-      int q = me;
+    // sources polled together (P <= N*MAXG ranks: at most N*MAXG-1 sources),
+    // and KU units per thread per round when the tile is small: a thread with
+    // several units waits one poll round trip per KU units, not per unit
+    constexpr int kGrp = N * MAXG - 1 < 1 ? 1 : (N * MAXG - 1 > 8 ? 8 : N * MAXG - 1);
+    constexpr int KU = kGrp <= 4 ? 2 : 1;
+    for (uint64_t u0 = ub + threadIdx.x; u0 < ue; u0 += static_cast<uint64_t>(blockDim.x) * KU) {
+      uint64_t uk[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) uk[k] = u0 + static_cast<uint64_t>(k) * blockDim.x;
       for (int j0 = 1; j0 < P; j0 += kGrp) {
-        uint32_t r[1][kGrp][RDW];
-        uint4* slots[1][kGrp];
-        int qs[1][kGrp];
-        int valid[kGrp];
+        uint32_t r[KU][kGrp][RDW];
+        uint4* slots[KU][kGrp];
+        int qs[KU][kGrp];
+        int valid[KU][kGrp];
         uint32_t pending = 0;
 #pragma unroll
-        for (int t = 0; t < kGrp; ++t) {
-          valid[t] = 0;
-          qs[0][t] = q;
-          slots[0][t] = reinterpret_cast<uint4*>(b_mine);
-          if (j0 + t < P) {
-            q = q == 0 ? P - 1 : q - 1;
-            qs[0][t] = q;
-            slots[0][t] = reinterpret_cast<uint4*>(b_mine + static_cast<uint64_t>(q) * b_stride);
-            const uint32_t e0 = static_cast<uint32_t>(q * SP) + UE * static_cast<uint32_t>(u);
-            valid[t] = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
-            if (valid[t] > 0) {
-              pending |= 1u << t;
-              prefetch_resid<E>(resid, e0);
+        for (int k = 0; k < KU; ++k) {
+#pragma unroll
+          for (int t = 0; t < kGrp; ++t) {
+            int q = me - (j0 + t);
+            if (q < 0) q += P;
+            valid[k][t] = 0;
+            qs[k][t] = q;
+            slots[k][t] = reinterpret_cast<uint4*>(b_mine + static_cast<uint64_t>(q) * b_stride);
+            if (j0 + t < P && uk[k] < ue) {
+              const uint32_t e0 = static_cast<uint32_t>(q * SP) + UE * static_cast<uint32_t>(uk[k]);
+              valid[k][t] = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
+              if (valid[k][t] > 0) {
+                pending |= 1u << (k * kGrp + t);
+                prefetch_resid<E>(resid, e0);
+              }
             }
           }
         }
-        recv_grid<Raw, RDW, 1, kGrp>(c, slots, u, r, pending, qs);
+        recv_rows<Raw, RDW, KU, kGrp>(c, slots, uk, r, pending, qs);
 #pragma unroll
-        for (int t = 0; t < kGrp; ++t) {
-          if (valid[t] > 0) {
-            emit<E, UE>(recv, resid, static_cast<uint32_t>(qs[0][t] * SP) + UE * static_cast<uint32_t>(u),
-                             valid[t], r[0][t]);
+        for (int k = 0; k < KU; ++k) {
+#pragma unroll
+          for (int t = 0; t < kGrp; ++t) {
+            if (valid[k][t] > 0) {
+              emit<E, UE>(recv, resid,
+                          static_cast<uint32_t>(qs[k][t] * SP) + UE * static_cast<uint32_t>(uk[k]),
+                          valid[k][t], r[k][t]);
+            }
           }
         }
       }

@@ -79,7 +79,10 @@ __global__ void canary_kernel(const __grid_constant__ LaunchParams lp, int peer,
     const uint4 v = ld_volatile16(mine);
     const bool empty = (v.x & v.y & v.z & v.w) == 0xFFFFFFFFu;
     if (!empty && (v.y != v.w || v.x != v.y * K || v.z != v.w * K)) ++torn;
-    if (v.y == last && v.w == last) break;
+    // done at this run's last flag — or past it: the writer does not wait for
+    // the reader, so it may already be streaming its next run's cells (flags
+    // grow run to run; those observations are checked the same way)
+    if (!empty && v.y == v.w && static_cast<int32_t>(v.y - last) >= 0) break;
     if (jitter_ns) __nanosleep(mix32(seed ^ spins) % jitter_ns);
     if ((spins & 255u) == 0u && globaltimer() > t_limit) {
       out[0] = ~0u;
