@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--graph", action="store_true", help="capture runs of calls in CUDA graphs")
     ap.add_argument("--sync-every", type=int, default=1)
     ap.add_argument("--multicast", action="store_true", help="also the NVLS one-shot")
+    ap.add_argument("--registered", action="store_true",
+                    help="also in-place all-reduces of registered buffers")
+    ap.add_argument("--jitter", type=int, default=0, help="injected delays up to this many ns")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -46,6 +49,13 @@ def main():
             algos.append("mcast")
     # call kinds: the all-reduce, its fused residual epilogue, the ring / tree orders
     kinds = ["allreduce", "allreduce", "residual", "ring", "tree"]
+    regbuf = {}
+    if args.registered:
+        kinds.append("registered")
+        for dt in (torch.bfloat16, torch.float32, torch.int32):
+            regbuf[dt] = comm.alloc_symmetric(1 << 20, dt)
+    if args.jitter:
+        comm.set_jitter(args.jitter, 77 + rank)
     dtypes = [torch.bfloat16, torch.float32, torch.int32]
     total = world * (world + 1) // 2
     bad = 0
@@ -73,6 +83,10 @@ def main():
             comm.ring_allreduce(x, y)
         elif kind == "tree":
             comm.tree_allreduce(x, y)
+        elif kind == "registered":
+            buf = regbuf[dt][:n]
+            buf.copy_(x)
+            comm.allreduce_registered(buf, y)
         else:
             comm.allreduce(x, y)
         pending.append((it, f"{kind}:{algo}", blocks, dt, n, idx, y, resid))
