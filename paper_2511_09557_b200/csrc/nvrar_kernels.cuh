@@ -720,8 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   // units; and this rank's own units of the NEXT round are loaded one round
   // ahead, so it does not wait for an HBM load per unit either (tiles up to 8
   // sources; with 16 the extra live registers would spill).
-  // (Lamport cells only: the LL protocol's two cells per unit would spill)
-  constexpr int KU = LAMPORT && N * MAXG <= 4 ? 2 : 1;
+  constexpr int KU = N * MAXG <= 4 ? 2 : 1;
   constexpr bool kOwnAhead = N * MAXG <= 8;
   const bool tree = order == kOrderTree;
   uint32_t own_next[KU][RDW];
