@@ -715,183 +715,135 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
                           static_cast<uint64_t>(parity) * d.world * d.lay.a_src * 8;
   const uint64_t a_stride = d.lay.a_src * 8;
   uint64_t len_seen = 0;
-  // KU units per thread per round (small tiles): their sources are polled
-  // together, so a thread with several units waits one poll round trip per KU
-  // units; and this rank's own units of the NEXT round are loaded one round
-  // ahead, so it does not wait for an HBM load per unit either (tiles up to 8
-  // sources; with 16 the extra live registers would spill).
-  constexpr int KU = N * MAXG <= 4 ? 2 : 1;
+  // this rank's own unit of the NEXT iteration is loaded one iteration ahead,
+  // so a thread with several units does not wait for an HBM load per unit
+  // (small tiles only: with 16 sources the extra live registers spill)
   constexpr bool kOwnAhead = N * MAXG <= 8;
-  const bool tree = order == kOrderTree;
-  uint32_t own_next[KU][RDW];
+  uint32_t own_next[RDW];
 #pragma unroll
-  for (int k = 0; k < KU; ++k) {
+  for (int q = 0; q < RDW; ++q) own_next[q] = pre[0][q];
+  for (uint64_t u = ub + threadIdx.x; u < ue; u += blockDim.x) {
+    const uint32_t e0 = mybase + UE * static_cast<uint32_t>(u);
+    const int valid = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0));
+    uint32_t own[RDW];
+    if constexpr (kOwnAhead) {
 #pragma unroll
-    for (int q = 0; q < RDW; ++q) own_next[k][q] = pre[0][q];
-  }
-  if (kOwnAhead && KU > 1) {
-    // the rest of the first round (unit 0 came with the prefetch)
-#pragma unroll
-    for (int k = 1; k < KU; ++k) {
-      const uint64_t u = u_first + static_cast<uint64_t>(k) * blockDim.x;
-      const uint32_t e1 = mybase + UE * static_cast<uint32_t>(u);
-      const int v1 = u < ue ? clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e1)) : 0;
-      if (v1 > 0) load_raw<E, UE>(send, e1, v1, own_next[k]);
-    }
-  }
-  for (uint64_t u0 = ub + threadIdx.x; u0 < ue; u0 += static_cast<uint64_t>(blockDim.x) * KU) {
-    uint64_t uk[KU];
-    uint32_t e0[KU], eg0[KU];
-    int valid[KU], c0[KU];
-    bool straddle[KU];
-    uint32_t own[KU][RDW];
-#pragma unroll
-    for (int k = 0; k < KU; ++k) {
-      uk[k] = u0 + static_cast<uint64_t>(k) * blockDim.x;
-      e0[k] = mybase + UE * static_cast<uint32_t>(uk[k]);
-      valid[k] = uk[k] < ue ? clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e0[k])) : 0;
-      if constexpr (kOwnAhead) {
-#pragma unroll
-        for (int q = 0; q < RDW; ++q) own[k][q] = own_next[k][q];
-        const uint64_t un = uk[k] + static_cast<uint64_t>(blockDim.x) * KU;
-        if (un < ue) {
-          const uint32_t e1 = mybase + UE * static_cast<uint32_t>(un);
-          const int v1 = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e1));
-          if (v1 > 0) load_raw<E, UE>(send, e1, v1, own_next[k]);
-        }
+      for (int q = 0; q < RDW; ++q) own[q] = own_next[q];
+      if (u + blockDim.x < ue) {
+        const uint32_t e1 = e0 + UE * blockDim.x;
+        const int v1 = clamp_valid<UE>(static_cast<int64_t>(n32) - static_cast<int64_t>(e1));
+        if (v1 > 0) load_raw<E, UE>(send, e1, v1, own_next);
       }
     }
-    if (valid[0] == 0 && (KU == 1 || valid[KU - 1] == 0)) continue;
+    if (valid == 0) continue;
+    prefetch_resid<E>(resid, e0);
+    const bool tree = order == kOrderTree;
+    const uint32_t eg0 = e0 + e_off;  // index in the whole vector (the order's frame)
+    // the tree chain does not depend on the chunk: one fixed order
+    const int c0 = tree ? 0 : static_cast<int>(eg0 / SG32);
+    const bool straddle = NVRAR_UNLIKELY(
+        !tree && eg0 + static_cast<uint32_t>(valid) - 1u >= static_cast<uint32_t>(c0 + 1) * SG32);
+    int l0 = tree ? OG - 1 : c0 + 1;
+    if (l0 >= OG) l0 -= OG;
 
-    // Every source's unit, in fold order: row k*N+nn, column j is unit uk[k]'s
-    // copy from member (c0+1+j) % OG of node nn (tree: member OG-1-j; ring: the
-    // rank at ring position (c0+1+j) % P).
-    uint32_t r[KU * N][MAXG][RDW];
-    uint4* slots[KU * N][MAXG];
-    int src[KU * N][MAXG];
-    uint64_t urow[KU * N];
+    // Every source's unit, in fold order: r[nn][j] is the copy of member
+    // (c0+1+j) % OG of node nn (tree: member OG-1-j; ring: the rank at ring
+    // position (c0+1+j) % P).
+    uint32_t r[N][MAXG][RDW];
+    uint4* slots[N][MAXG];
+    int src[N][MAXG];
     uint32_t pending = 0;
 #pragma unroll
-    for (int k = 0; k < KU; ++k) {
-      prefetch_resid<E>(valid[k] > 0 ? resid : nullptr, e0[k]);
-      eg0[k] = e0[k] + e_off;  // index in the whole vector (the order's frame)
-      // the tree chain does not depend on the chunk: one fixed order
-      c0[k] = tree ? 0 : static_cast<int>(eg0[k] / SG32);
-      straddle[k] = NVRAR_UNLIKELY(valid[k] > 0 && !tree &&
-                                   eg0[k] + static_cast<uint32_t>(valid[k]) - 1u >=
-                                       static_cast<uint32_t>(c0[k] + 1) * SG32);
-      int l0 = tree ? OG - 1 : c0[k] + 1;
-      if (l0 >= OG) l0 -= OG;
+    for (int nn = 0; nn < N; ++nn) {
+      int l = l0;
 #pragma unroll
-      for (int nn = 0; nn < N; ++nn) {
-        const int row = k * N + nn;
-        urow[row] = uk[k];
-        int l = l0;
+      for (int j = 0; j < MAXG; ++j) {
+        src[nn][j] = order == kOrderRing ? static_cast<int>(lp.perm[l & 63]) : nn * G + l;
+        slots[nn][j] = reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(src[nn][j]) * a_stride);
+        if (j < OG) {
+          const int s = src[nn][j];
+          if (s == me) {
+            if constexpr (kOwnAhead) {
 #pragma unroll
-        for (int j = 0; j < MAXG; ++j) {
-          src[row][j] = order == kOrderRing ? static_cast<int>(lp.perm[l & 63]) : nn * G + l;
-          slots[row][j] = reinterpret_cast<uint4*>(a_mine + static_cast<uint64_t>(src[row][j]) * a_stride);
-          if (j < OG) {
-            const int sr = src[row][j];
-            if (valid[k] == 0) {
-              // no unit here (past the end): nothing to wait for
-            } else if (sr == me) {
-              if constexpr (kOwnAhead) {
+              for (int q = 0; q < RDW; ++q) r[nn][j][q] = own[q];
+            } else if (u == u_first) {
 #pragma unroll
-                for (int q = 0; q < RDW; ++q) r[row][j][q] = own[k][q];
-              } else if (uk[k] == u_first) {
-#pragma unroll
-                for (int q = 0; q < RDW; ++q) r[row][j][q] = pre[0][q];
-              } else {
-                load_raw<E, UE>(send, e0[k], valid[k], r[row][j]);
-              }
+              for (int q = 0; q < RDW; ++q) r[nn][j][q] = pre[0][q];
             } else {
-              pending |= 1u << (row * MAXG + j);
+              load_raw<E, UE>(send, e0, valid, r[nn][j]);
             }
-            l = tree ? l - 1 : (l + 1 == OG ? 0 : l + 1);
+          } else {
+            pending |= 1u << (nn * MAXG + j);
           }
+          l = tree ? l - 1 : (l + 1 == OG ? 0 : l + 1);
         }
       }
     }
-    recv_rows<Raw, RDW, KU * N, MAXG>(c, slots, urow, r, pending, src);
-    if (lazy_len && u0 == u_first && threadIdx.x < P) {
+    recv_grid<Raw, RDW, N, MAXG>(c, slots, u, r, pending, src);
+    if (lazy_len && u == u_first && threadIdx.x < P) {
       // the peer's (seq, len) word, read now that its data is here; used at the end
       len_seen = ld_volatile64(counters(d, me) + threadIdx.x);
     }
+    const int c3 = straddle ? c0 + 1 : c0;
 
+    // Node partials, combined on the fly into the pairwise tree over nodes
+    // (node order == the XOR-step adds): stack[k] holds a finished subtree of
+    // 2^k nodes.
+    A stack[kLevels][UE];
 #pragma unroll
-    for (int k = 0; k < KU; ++k) {
-      if (valid[k] == 0) continue;
-      const int c3 = straddle[k] ? c0[k] + 1 : c0[k];
-      // this unit's tile
-      uint32_t rt[N][MAXG][RDW];
+    for (int nn = 0; nn < N; ++nn) {
+      A v[UE];
+      if (NVRAR_LIKELY(c0 == c3)) {
+        raw_to_acc<UE>(E{}, r[nn][0], v);
 #pragma unroll
-      for (int nn = 0; nn < N; ++nn) {
+        for (int j = 1; j < MAXG; ++j) {
+          if (j < OG) {
+            A a[UE];
+            raw_to_acc<UE>(E{}, r[nn][j], a);
 #pragma unroll
-        for (int j = 0; j < MAXG; ++j) {
-#pragma unroll
-          for (int q = 0; q < RDW; ++q) rt[nn][j][q] = r[k * N + nn][j][q];
+            for (int q = 0; q < UE; ++q) v[q] = acc_add(v[q], a[q]);
+          }
         }
-      }
-      // Node partials, combined on the fly into the pairwise tree over nodes
-      // (node order == the XOR-step adds): stack[m] holds a finished subtree of
-      // 2^m nodes.
-      A stack[kLevels][UE];
+      } else {
+        // The unit straddles a shard boundary: per-element fold order.
 #pragma unroll
-      for (int nn = 0; nn < N; ++nn) {
-        A v[UE];
-        if (NVRAR_LIKELY(c0[k] == c3)) {
-          raw_to_acc<UE>(E{}, rt[nn][0], v);
+        for (int q = 0; q < UE; ++q) {
+          const int cq = q < valid ? static_cast<int>((eg0 + q) / SG32) : c0;
+          const int rot = cq - c0;
+          A x = pick<E, UE, RDW, N, MAXG>(r, nn, rot % OG, q);
 #pragma unroll
           for (int j = 1; j < MAXG; ++j) {
-            if (j < OG) {
-              A a[UE];
-              raw_to_acc<UE>(E{}, rt[nn][j], a);
-#pragma unroll
-              for (int q = 0; q < UE; ++q) v[q] = acc_add(v[q], a[q]);
-            }
+            if (j < OG) x = acc_add(x, pick<E, UE, RDW, N, MAXG>(r, nn, (j + rot) % OG, q));
           }
-        } else {
-          // The unit straddles a shard boundary: per-element fold order.
-#pragma unroll
-          for (int q = 0; q < UE; ++q) {
-            const int cq = q < valid[k] ? static_cast<int>((eg0[k] + q) / SG32) : c0[k];
-            const int rot = cq - c0[k];
-            A x = pick<E, UE, RDW, N, MAXG>(rt, nn, rot % OG, q);
-#pragma unroll
-            for (int j = 1; j < MAXG; ++j) {
-              if (j < OG) x = acc_add(x, pick<E, UE, RDW, N, MAXG>(rt, nn, (j + rot) % OG, q));
-            }
-            v[q] = x;
-          }
-        }
-        int lvl = 0;
-#pragma unroll
-        for (int m = 0; m < kLevels - 1; ++m) {
-          if (((nn >> m) & 1) && lvl == m) {
-#pragma unroll
-            for (int q = 0; q < UE; ++q) v[q] = acc_add(stack[m][q], v[q]);
-            lvl = m + 1;
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < kLevels; ++m) {
-          if (m == lvl) {
-#pragma unroll
-            for (int q = 0; q < UE; ++q) stack[m][q] = v[q];
-          }
+          v[q] = x;
         }
       }
-      uint32_t o[RDW];
-      acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
-      emit<E, UE>(recv, resid, e0[k], valid[k], o);
-      if (!oneshot) {
-        jitter(c, 3 + static_cast<uint32_t>(uk[k] >> 5) * 64);
-        int q = me;
-        for (int j = 1; j < P; ++j) {
-          q = q + 1 == P ? 0 : q + 1;
-          Raw::template put<RDW>(slot_b(d, q, parity, me), uk[k], o, c.seq);
+      int lvl = 0;
+#pragma unroll
+      for (int k = 0; k < kLevels - 1; ++k) {
+        if (((nn >> k) & 1) && lvl == k) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) v[q] = acc_add(stack[k][q], v[q]);
+          lvl = k + 1;
         }
+      }
+#pragma unroll
+      for (int k = 0; k < kLevels; ++k) {
+        if (k == lvl) {
+#pragma unroll
+          for (int q = 0; q < UE; ++q) stack[k][q] = v[q];
+        }
+      }
+    }
+    uint32_t o[RDW];
+    acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
+    emit<E, UE>(recv, resid, e0, valid, o);
+    if (!oneshot) {
+      jitter(c, 3 + static_cast<uint32_t>(u >> 5) * 64);
+      int q = me;
+      for (int j = 1; j < P; ++j) {
+        q = q + 1 == P ? 0 : q + 1;
+        Raw::template put<RDW>(slot_b(d, q, parity, me), u, o, c.seq);
       }
     }
   }
