@@ -149,7 +149,15 @@ struct LaunchParams {
 //   prefetch-size hint (set for pinned host inputs read over PCIe).
 // kFlagSeqBarrier: thread 0 alone reads the call number and a __syncthreads
 //   broadcasts it (the round-1 prologue; default: every thread reads it).
-enum : int { kFlagEarlySeq = 1, kFlagLazyLen = 2, kFlagL2Fetch256 = 4, kFlagSeqBarrier = 8 };
+// kFlagDirectStream: the direct schedule stores its outputs evict-first
+//   (st.global.cs) — an A/B knob.
+enum : int {
+  kFlagEarlySeq = 1,
+  kFlagLazyLen = 2,
+  kFlagL2Fetch256 = 4,
+  kFlagSeqBarrier = 8,
+  kFlagDirectStream = 16
+};
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):
 //   NVRAR — ring fold of the node's ranks per G-chunk, pairwise tree over nodes;

@@ -944,6 +944,7 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   const uint32_t SG = (n_ord + G - 1) / G;  // order in the whole vector's frame
   const uint32_t e_off = static_cast<uint32_t>(lp.e_off);
   const bool l2pf = (lp.flags & kFlagL2Fetch256) != 0;
+  const bool stream_st = (lp.flags & kFlagDirectStream) != 0;
   const uint32_t U = (n + UE - 1) / UE;
   const uint32_t slice = (U + P - 1) / P;
   // small vectors leave the last ranks' slices empty (s0 clamps to U)
@@ -1053,7 +1054,20 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
     acc_to_raw<UE>(E{}, stack[kLevels - 1], o);
     u += blockDim.x;
     if (u < ue) load_unit(u);
-    for (int r2 = 0; r2 < P; ++r2) emit<E, UE>(lp.recv[r2], lp.resid[r2], e0, valid, o);
+    if (stream_st && valid == UE && lp.resid[0] == nullptr) {
+      // experiment (kFlagDirectStream): evict-first stores of the P outputs
+      for (int r2 = 0; r2 < P; ++r2) {
+        uint8_t* at = static_cast<uint8_t*>(lp.recv[r2]) + static_cast<uint64_t>(e0) * E::kBytes;
+        if ((reinterpret_cast<uintptr_t>(at) & 15u) == 0) {
+          asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(at), "r"(o[0]), "r"(o[1]),
+                       "r"(o[2]), "r"(o[3]));
+        } else {
+          emit<E, UE>(lp.recv[r2], lp.resid[r2], e0, valid, o);
+        }
+      }
+    } else {
+      for (int r2 = 0; r2 < P; ++r2) emit<E, UE>(lp.recv[r2], lp.resid[r2], e0, valid, o);
+    }
   }
   stamp(d, 6);
 }
