@@ -387,8 +387,7 @@ int nvrar_comm_create(const nvrar_init_args* a, nvrar_comm_t* out) {
   if (const char* v = getenv("NVRAR_HOST_L2FETCH")) c->host_l2fetch = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_DEV_L2FETCH")) c->dev_l2fetch = atoi(v) != 0;
   if (const char* v = getenv("NVRAR_FLAGS")) {
-    c->flags = atoi(v) & (kFlagEarlySeq | kFlagLazyLen | kFlagSeqBarrier | kFlagDirectStream |
-                                kFlagPreWaitSeq);
+    c->flags = atoi(v) & (kFlagEarlySeq | kFlagLazyLen | kFlagSeqBarrier | kFlagDirectStream);
   }
   if (const char* v = getenv("NVRAR_THREADS")) {
     const int t = atoi(v);

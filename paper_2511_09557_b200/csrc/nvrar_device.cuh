@@ -151,16 +151,12 @@ struct LaunchParams {
 //   broadcasts it (the round-1 prologue; default: every thread reads it).
 // kFlagDirectStream: the direct schedule stores its outputs evict-first
 //   (st.global.cs) — an A/B knob.
-// kFlagPreWaitSeq: every kernel lets the next launch start only after its
-//   call-number write-back (fence + griddepcontrol.launch_dependents), so the
-//   next kernel reads the call number BEFORE griddepcontrol.wait — an A/B knob.
 enum : int {
   kFlagEarlySeq = 1,
   kFlagLazyLen = 2,
   kFlagL2Fetch256 = 4,
   kFlagSeqBarrier = 8,
-  kFlagDirectStream = 16,
-  kFlagPreWaitSeq = 32
+  kFlagDirectStream = 16
 };
 
 // Reduction orders the flat kernel evaluates (the reference's three collectives):

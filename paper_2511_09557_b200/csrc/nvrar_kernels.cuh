@@ -79,18 +79,11 @@ __device__ __forceinline__ const RankDesc& rank_desc(const LaunchParams& lp) {
 
 // Prologue, part 1: wait for the previous kernel on the stream (the previous
 // call, or the producer of our input) and let the next launch start early.
-__device__ __forceinline__ void begin_wait(const RankDesc& d, int flags = 0) {
+__device__ __forceinline__ void begin_wait(const RankDesc& d) {
   stamp(d, 0);
   pdl_wait();
-  if (!(flags & kFlagPreWaitSeq)) pdl_launch_dependents();
+  pdl_launch_dependents();
   stamp(d, 7);
-}
-// kFlagPreWaitSeq: the dependent launch is released after the write-back
-__device__ __forceinline__ void trigger_after_seq(int flags) {
-  if (flags & kFlagPreWaitSeq) {
-    __threadfence();
-    pdl_launch_dependents();
-  }
 }
 
 // The call number and the sticky fault word of this CTA. Only this GPU's
@@ -153,7 +146,7 @@ __device__ __forceinline__ bool begin_seq(const RankDesc& d, Ctl& c, int flags =
 
 // CTA b owns slots b, b + grid, ...; warp 0 writes them (small grids own many).
 // The caller guarantees every warp of the CTA has read slot b already.
-__device__ __forceinline__ void write_seq_slots(const RankDesc& d, uint32_t seq, int flags = 0) {
+__device__ __forceinline__ void write_seq_slots(const RankDesc& d, uint32_t seq) {
 #ifdef NVRAR_ABL_NO_END  // experiment builds only (tools/ablate.sh): no counter write-back
   return;
 #endif
@@ -162,14 +155,13 @@ __device__ __forceinline__ void write_seq_slots(const RankDesc& d, uint32_t seq,
          i += 32 * gridDim.x) {
       d.state->seq[i] = seq;
     }
-    trigger_after_seq(flags);
   }
 }
 
-__device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq, int flags = 0) {
+__device__ __forceinline__ void end_call(const RankDesc& d, uint32_t seq) {
   // every warp of the CTA has read slot b (seq_issue) before it is rewritten
   __syncthreads();
-  write_seq_slots(d, seq, flags);
+  write_seq_slots(d, seq);
   stamp(d, 6);
 }
 
@@ -271,11 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
 #pragma unroll
   for (int j = 0; j < MG; ++j) grp[j] = local + j >= G ? local + j - G : local + j;
 
-  const bool pre_seq = (lp.flags & kFlagPreWaitSeq) != 0;
-  SeqWords sw{0u, 0u};
-  if (pre_seq) sw = seq_issue(d, lp.flags);
-  begin_wait(d, lp.flags);
-  if (!pre_seq) sw = seq_issue(d, lp.flags);
+  begin_wait(d);
+  const SeqWords sw = seq_issue(d, lp.flags);
   // Prefetch this thread's first unit of every chunk while the call number is
   // read (the loads do not depend on it): pre[j] = chunk (local + j) % G.
   uint32_t pre[MG][RDW];
@@ -292,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
   Ctl c;
   if (!begin_seq(d, c, sw, lp.flags)) return;  // sticky fault: comm is dead
   const uint32_t parity = c.seq & 1u;
-  if (lp.flags & kFlagEarlySeq) end_call(d, c.seq, lp.flags);
+  if (lp.flags & kFlagEarlySeq) end_call(d, c.seq);
 
   // Peer-only sync, publish half (nvrar.hpp:163-171).
   if (kSteps > 0 && blockIdx.x == 0 && threadIdx.x < kSteps) {
@@ -536,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) hier_kernel(const __grid_constant
     }
   }
   stamp(d, 5);
-  if (!(lp.flags & kFlagEarlySeq)) end_call(d, c.seq, lp.flags);
+  if (!(lp.flags & kFlagEarlySeq)) end_call(d, c.seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -600,12 +589,9 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   const void* resid = EMU ? lp.resid[blockIdx.y] : lp.resid[0];
   const uint64_t u_first = ub + threadIdx.x;
 
-  const bool pre_seq = (lp.flags & kFlagPreWaitSeq) != 0;
-  SeqWords sw{0u, 0u};
-  if (pre_seq) sw = seq_issue(d, lp.flags);
-  begin_wait(d, lp.flags);
+  begin_wait(d);
   // the call-number load first: its latency overlaps the input prefetch
-  if (!pre_seq) sw = seq_issue(d, lp.flags);
+  const SeqWords sw = seq_issue(d, lp.flags);
   // Prefetch this thread's first unit of every sub-shard (pre[j]: owner
   // (me + j) % P; j = 0 is our own) before the call number is read. One-shot
   // sends the same unit to everyone, so it loads once.
@@ -625,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
   if (!begin_seq(d, c, sw, lp.flags)) return;
   const uint32_t parity = c.seq & 1u;
   const bool lazy_len = !EMU && (lp.flags & kFlagLazyLen) != 0;
-  if (lp.flags & kFlagEarlySeq) end_call(d, c.seq, lp.flags);
+  if (lp.flags & kFlagEarlySeq) end_call(d, c.seq);
   if (lazy_len) {
     c.len_words = counters(d, me);
     c.len = static_cast<uint32_t>(n);
@@ -715,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
 #ifndef NVRAR_ABL_NO_SYNC2  // experiment builds only (tools/ablate.sh)
     __syncthreads();
 #endif
-    if (seq_mid) write_seq_slots(d, c.seq, lp.flags);
+    if (seq_mid) write_seq_slots(d, c.seq);
   }
   stamp(d, 3);
   c.phase = 4;
@@ -933,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1) flat_kernel(const __grid_constant
     }
   }
   stamp(d, 5);
-  if (!(lp.flags & kFlagEarlySeq) && !seq_mid) end_call(d, c.seq, lp.flags);
+  if (!(lp.flags & kFlagEarlySeq) && !seq_mid) end_call(d, c.seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -951,7 +937,7 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
   const RankDesc& d = *lp.desc[blockIdx.y];
   // the descriptor is immutable while calls run: read it before the wait
   RankState* const st = d.state;
-  begin_wait(d, lp.flags);
+  begin_wait(d);
   const uint32_t n = static_cast<uint32_t>(lp.count);
   const int G = lp.d0.gpus, P = lp.nlocal;  // param space: no dependent load
   const uint32_t n_ord = lp.n_order ? static_cast<uint32_t>(lp.n_order) : n;
@@ -977,7 +963,6 @@ __global__ void __launch_bounds__(kDirectThreads) direct_kernel(const __grid_con
          i += 32 * gridDim.x) {
       atomicAdd(&st->seq[i], 1u);
     }
-    trigger_after_seq(lp.flags);
   }
   uint32_t r[N][MAXG][RDW];
   // loads of unit u from every rank, in each node's fold order (starting at the
@@ -1107,13 +1092,9 @@ __global__ void __launch_bounds__(kThreads, 1) pull_kernel(const __grid_constant
   constexpr int RDW = 4;
   constexpr int kLevels = Log2<N>::value + 1;
   const RankDesc& d = lp.d0;
-  const bool pre_seq = (lp.flags & kFlagPreWaitSeq) != 0;
-  SeqWords sw{0u, 0u};
-  if (pre_seq) sw = seq_issue(d, lp.flags);
-  begin_wait(d, lp.flags);
-  if (!pre_seq) sw = seq_issue(d, lp.flags);
+  begin_wait(d);
   Ctl c;
-  if (!begin_seq(d, c, sw, lp.flags)) return;
+  if (!begin_seq(d, c, lp.flags)) return;
   const int P = d.world, me = d.rank, G = d.gpus;
   const uint32_t n = static_cast<uint32_t>(lp.count);
   const uint32_t SG = (n + G - 1) / G;
@@ -1229,7 +1210,7 @@ __global__ void __launch_bounds__(kThreads, 1) pull_kernel(const __grid_constant
       }
     }
   }
-  end_call(d, c.seq, lp.flags);
+  end_call(d, c.seq);
 }
 
 template <class E>
