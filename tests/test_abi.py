@@ -159,6 +159,51 @@ def test_local_group_buffers_must_be_uniform():
         _check_uniform(a[:3] + [torch.zeros(16, dtype=torch.bfloat16)], a)
 
 
+def test_local_group_launch_host_checks_every_buffer():
+    """LocalGroup.launch_host's one-pass checks (no device: the C call is a
+    stub that records its arguments): every rank's pair is checked for length,
+    dtype, device and layout, and the pointers reach the C ABI in rank order."""
+    import ctypes
+
+    import torch
+    from paper_2511_09557_b200.comm import InvalidArgumentError, LocalGroup
+
+    p = 4
+    seen = {}
+
+    class Lib:
+        def nvrar_allreduce_local_host(self, arr, np_, send, recv, n, dt, op, stream):
+            seen.update(p=np_, send=[send[i] for i in range(np_)],
+                        recv=[recv[i] for i in range(np_)], n=n, dt=dt)
+            return 0
+
+    g = LocalGroup.__new__(LocalGroup)
+    g.comms = [None] * p
+    g._lib = Lib()
+    g._arr = (ctypes.c_void_p * p)()
+    g._ptrs, g._ptr_fmt = ctypes.c_void_p * p, f"{p}Q"
+    ins = [torch.zeros(16) for _ in range(p)]
+    outs = [torch.zeros(16) for _ in range(p)]
+
+    class S:
+        cuda_stream = 0
+
+    g.launch_host(ins, outs, stream=S())
+    assert seen["send"] == [t.data_ptr() for t in ins]
+    assert seen["recv"] == [t.data_ptr() for t in outs]
+    assert seen["n"] == 16 and seen["p"] == p
+    bad = [
+        (ins, outs[:3] + [torch.zeros(15)]),                      # a short output
+        (ins[:2] + [torch.zeros(15), ins[3]], outs),               # a short input
+        (ins, outs[:3] + [torch.zeros(16, dtype=torch.bfloat16)]),  # another dtype
+        (ins[:3] + [torch.zeros(32)[::2]], outs),                  # not contiguous
+        (ins[:3], outs[:3]),                                       # a rank missing
+    ]
+    for a, b in bad:
+        with pytest.raises(InvalidArgumentError):
+            g.launch_host(a, b, stream=S())
+
+
 def test_torch_op_ids_are_never_reused():
     """unregister + register must not hand out a live id again."""
     from paper_2511_09557_b200 import torch_op
