@@ -166,7 +166,9 @@ int nvrar_finalize(nvrar_comm_t comm);
  * can use any bootstrap: nvrar_register_buffer exports this rank's range
  * (any range inside a cudaMalloc allocation) as an opaque handle and returns
  * its id; after an all-gather of the handles, nvrar_connect_buffer maps every
- * peer's range (CUDA IPC; same-process ranks directly). Symmetric: every rank
+ * peer's range (CUDA IPC; same-process ranks directly) — once per
+ * registration (a second call, or one after a failed call, is
+ * INVALID_ARGUMENT: deregister and register again). Symmetric: every rank
  * registers the same number of bytes, in the same order (ids then agree).
  * Registered inputs can be all-reduced in place (nvrar_allreduce_registered);
  * nvrar_buffer_peer_ptr gives the caller peer rank p's range as mapped here.

@@ -639,6 +639,10 @@ int nvrar_connect_buffer(nvrar_comm_t c, int buf, const nvrar_handle_t* hs, int 
   if (!c || !hs) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "null argument");
   nvrar_comm::RegBuf* r = find_reg(c, buf);
   if (!r) return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "no registered buffer %d", buf);
+  if (r->connected || !r->opened.empty()) {
+    // a second connect would map the peers again (and leak the first mappings)
+    return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "buffer %d is already connected", buf);
+  }
   if (count != c->world) {
     return fail(c, NVRAR_ERR_INVALID_ARGUMENT, "expected %d handles, got %d", c->world, count);
   }

@@ -214,6 +214,10 @@ def registered(comm, rank, nodes, gpus, device, log):
     if world > 1 and comm.buffer_peer_ptr(1, peer) == 0:
         fails += 1
         log("no peer mapping for registered buffer 1")
+    # a connected registration is never mapped a second time
+    if comm._lib.nvrar_connect_buffer(comm._h, 1, (L.Handle * world)(), world) == 0:
+        fails += 1
+        log("a second connect of registered buffer 1 was accepted")
     return fails
 
 
