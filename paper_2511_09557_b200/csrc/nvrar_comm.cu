@@ -882,7 +882,12 @@ static void resolve(nvrar_comm* c0, int nl, size_t count, int dtype, bool emu, i
     // host buffers over PCIe: at most 64 CTAs, so threads loop and the link
     // reads/writes of consecutive units overlap (measured at 1 MB: P=2
     // 63.8 -> 53.7 us, P=4 65.2 -> 57.0 us against 128 CTAs)
-    blocks = std::min(blocks, 64);
+    static const int host_ctas = [] {  // the cap (env NVRAR_HOST_CTAS; tuning knob)
+      const char* e = getenv("NVRAR_HOST_CTAS");
+      const int v = e ? atoi(e) : 64;
+      return v >= 1 && v <= kSeqSlots ? v : 64;
+    }();
+    blocks = std::min(blocks, host_ctas);
   }
   *algo_out = algo;
   *blocks_out = blocks;
